@@ -1,0 +1,122 @@
+/*
+ * tsm2x.h — C ABI of libtsm2x.so, the B200 (sm_100a) TSM2R / TSM2L tall-and-skinny GEMM.
+ *
+ * Semantics (all entry points):  C_out = C + A * B   (or C_out = A * B with TSM2X_FLAG_C_IS_ZERO)
+ *   A is m x k, B is k x n, C is m x n, all column-major with leading dimensions lda/ldb/ldc
+ *   (element (i, j) at ptr[i + j * ld]) — the storage convention of the reference `Matrix`
+ *   (reference pkg/src/tsgemm/core.py:84-91, flat index i + j*rows).
+ *   Naming follows the reference (m, k, n) with the skinny dimension n.
+ *
+ * Which reference interface each entry point replaces:
+ *   tsm2x_validate   <- tsgemm.kernels._check_dims            (pkg/src/tsgemm/kernels.py:36-44)
+ *                       tsgemm.core.KernelParams.__post_init__ (pkg/src/tsgemm/core.py:176-181)
+ *                       tsgemm.core.KernelParams.validate_for  (pkg/src/tsgemm/core.py:183-190)
+ *   tsm2x_run_host   <- tsgemm.kernels.run_native             (pkg/src/tsgemm/kernels.py:391-416)
+ *                       host buffers in, host buffer out (the reference's Matrix boundary);
+ *                       L_OPT2 zero-C rule of kernels.py:366-368 checked on the host copy.
+ *   tsm2x_run        <- the same operation on device-resident buffers, stream-ordered
+ *                       (the GPU-native form of run_native; no reference equivalent exists
+ *                       because the reference has no device — SURVEY.md §8b).
+ *   tsm2x_last_error <- the ValueError / RuntimeError message text.
+ *
+ * Return codes: 0 = OK; TSM2X_EINVAL maps to Python ValueError (same conditions as the
+ * reference), every other negative code maps to RuntimeError. Messages are thread-local.
+ * All entry points are re-entrant and thread-safe; device work is stream-ordered.
+ */
+#ifndef TSM2X_H_
+#define TSM2X_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSM2X_OK 0
+#define TSM2X_EINVAL (-1)      /* argument/shape/param/zero-C violation -> ValueError   */
+#define TSM2X_ECUDA (-2)       /* CUDA runtime failure                  -> RuntimeError */
+#define TSM2X_ENOMEM (-3)      /* device or pinned allocation failure   -> RuntimeError */
+#define TSM2X_EUNSUPPORTED (-4)/* no sm_100a device / unsupported case  -> RuntimeError */
+
+/* reference core.py:57-81 (Variant), same ordinal order as the enum definition */
+enum tsm2x_variant {
+  TSM2X_V0 = 0,      /* inner product, Alg 1                 */
+  TSM2X_V1 = 1,      /* outer product, Alg 2                 */
+  TSM2X_V2 = 2,      /* + shared-memory B tile, Alg 3        */
+  TSM2X_V3 = 3,      /* + prefetch (the TSM2R kernel), Alg 4 */
+  TSM2X_L_OPT1 = 4,  /* TSM2L row-tile loop, Alg 6           */
+  TSM2X_L_OPT2 = 5   /* TSM2L interleaved, zero C, Alg 7     */
+};
+
+/* reference core.py:23-46 (Precision) */
+enum tsm2x_precision { TSM2X_SINGLE = 0, TSM2X_DOUBLE = 1 };
+
+/* reference core.py:160-190 (KernelParams): t1 threads/block, t2 C columns per pass,
+ * t3 A elements per prefetch, tcf row tiles per thread (TSM2L); variant = the params' own
+ * variant field (validate_for rejects tcf > 1 unless it is a TSM2L variant). */
+typedef struct tsm2x_params {
+  int32_t t1, t2, t3, tcf;
+  int32_t variant;
+} tsm2x_params;
+
+/* flags */
+#define TSM2X_FLAG_C_IS_ZERO 0x1u   /* caller guarantees C == 0: C is written, never read  */
+#define TSM2X_FLAG_CHECK_ZERO_C 0x2u/* tsm2x_run + L_OPT2: verify C == 0 on the device
+                                       (synchronises the stream); EINVAL if not          */
+
+/* Kernel implementation override (tsm2x_run_ex); AUTO uses the B200 tuning table. */
+enum tsm2x_impl {
+  TSM2X_IMPL_AUTO = 0,
+  TSM2X_IMPL_STREAM_LDG = 1,  /* TSM2R: register-prefetched LDG.128 stream, stream-K split  */
+  TSM2X_IMPL_STREAM_TMA = 2,  /* TSM2R: bulk-copy (TMA engine) smem ring, warp-specialised  */
+  TSM2X_IMPL_TSM2L = 3,       /* TSM2L: whole B in smem, grid-stride row stream              */
+  TSM2X_IMPL_ABLATION = 4     /* the paper's V0/V1/V2 algorithms as written (ablation only)  */
+};
+
+/* Validation only (no device work): mirrors the reference's ValueError conditions. */
+int tsm2x_validate(int variant, int64_t m, int64_t k, int64_t n, const tsm2x_params* params);
+
+/* Device-resident run. A, B, C are device pointers; stream is a cudaStream_t (NULL = legacy
+ * default stream). Returns after enqueueing (asynchronous) unless CHECK_ZERO_C is set. */
+int tsm2x_run(int variant, int precision, int64_t m, int64_t k, int64_t n,
+              const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+              const tsm2x_params* params, uint32_t flags, void* stream);
+
+/* As tsm2x_run with an explicit implementation choice (benchmarks / ablations). */
+int tsm2x_run_ex(int variant, int precision, int64_t m, int64_t k, int64_t n,
+                 const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                 const tsm2x_params* params, uint32_t flags, int impl, void* stream);
+
+/* Host-buffer run (the drop-in for reference run_native): A (m x k, lda), B, C_in are host
+ * pointers (pinned or pageable); the result C_in + A*B is written to C_out (host, ldc; may
+ * alias C_in). H2D of A is pipelined with the kernels in column slabs (TSM2R) or row slabs
+ * (TSM2L). Synchronous. device = CUDA ordinal. */
+int tsm2x_run_host(int variant, int precision, int64_t m, int64_t k, int64_t n,
+                   const void* A, int64_t lda, const void* B, int64_t ldb,
+                   const void* C_in, void* C_out, int64_t ldc,
+                   const tsm2x_params* params, uint32_t flags, int device);
+
+/* Synthetic-input utility (not a reference interface): fills the rows x cols column-major
+ * block at ptr (leading dimension ld) with the counter-based uniform [0, 1) generator
+ *   x = splitmix64(seed * 0x9E3779B97F4A7C15 + ((col_offset + j) << 32 | (row_offset + i)))
+ *   u = (x >> 11) * 2^-53   (float64; cast to float32 for single, like Matrix.random)
+ * where (row_offset + i, col_offset + j) is the element's position in the full matrix, so
+ * any row slab or shard regenerates bit-identically on the host (oracle/rng.py). */
+int tsm2x_fill_uniform(int precision, int64_t rows, int64_t cols, void* ptr, int64_t ld, int64_t row_offset,
+                       int64_t col_offset, uint64_t seed, void* stream);
+
+/* Thread-local message describing the last non-OK return on this thread. */
+const char* tsm2x_last_error(void);
+
+/* Library version (major*10000 + minor*100 + patch) and build target ("sm_100a"). */
+int tsm2x_version(void);
+const char* tsm2x_build_target(void);
+
+/* Number of kernels this process has launched through the library since load (bench evidence). */
+int64_t tsm2x_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSM2X_H_ */

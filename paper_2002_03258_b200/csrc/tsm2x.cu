@@ -1,0 +1,812 @@
+// libtsm2x.so — C ABI (include/tsm2x.h), validation, kernel dispatch, workspace management and
+// the pipelined host-buffer path. Kernels live in the *.cuh files next to this one.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/tsm2x.h"
+#include "ablation.cuh"
+#include "common.cuh"
+#include "tsm2l.cuh"
+#include "tsm2r_stream.cuh"
+#include "tsm2r_tma.cuh"
+
+namespace tsm2x {
+
+// ------------------------------------------------------------------------------------------
+// errors
+static thread_local std::string t_err;
+static std::atomic<int64_t> g_launches{0};
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return code;
+}
+#define TSM2X_CUDA(expr)                                                                          \
+  do {                                                                                            \
+    cudaError_t e_ = (expr);                                                                      \
+    if (e_ != cudaSuccess) return fail(TSM2X_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+#define TSM2X_TRY(expr)        \
+  do {                         \
+    int rc_ = (expr);          \
+    if (rc_ != TSM2X_OK) return rc_; \
+  } while (0)
+
+static int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(TSM2X_ECUDA, "launch of %s failed: %s", what, cudaGetErrorString(e));
+  return TSM2X_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// validation — the reference's ValueError conditions, in the reference's order:
+//   dims positive (core.py:94-95 via Matrix), _check_dims (kernels.py:36-44),
+//   KernelParams.__post_init__ (core.py:176-181), validate_for (core.py:183-190).
+static int validate(int variant, int precision, int64_t m, int64_t k, int64_t n, const tsm2x_params* p) {
+  if (variant < TSM2X_V0 || variant > TSM2X_L_OPT2) return fail(TSM2X_EINVAL, "unknown kernel variant %d", variant);
+  if (precision != TSM2X_SINGLE && precision != TSM2X_DOUBLE)
+    return fail(TSM2X_EINVAL, "unknown precision %d; expected 0 (single) or 1 (double)", precision);
+  if (m < 1 || k < 1 || n < 1)
+    return fail(TSM2X_EINVAL, "matrix dimensions must be positive, got m=%lld k=%lld n=%lld", (long long)m,
+                (long long)k, (long long)n);
+  if (!p) return fail(TSM2X_EINVAL, "params must not be NULL");
+  const char* names[4] = {"t1", "t2", "t3", "tcf"};
+  const int32_t vals[4] = {p->t1, p->t2, p->t3, p->tcf};
+  for (int i = 0; i < 4; ++i)
+    if (vals[i] < 1) return fail(TSM2X_EINVAL, "%s must be >= 1, got %d", names[i], vals[i]);
+  if (p->t3 > p->t1) return fail(TSM2X_EINVAL, "t3 (%d) must not exceed t1 (%d)", p->t3, p->t1);
+  if ((int64_t)p->t2 > n) return fail(TSM2X_EINVAL, "t2 (%d) must not exceed n (%lld)", p->t2, (long long)n);
+  if (p->t1 % 32 != 0) return fail(TSM2X_EINVAL, "t1 (%d) must be a multiple of warp size 32", p->t1);
+  const bool params_tsm2l = p->variant == TSM2X_L_OPT1 || p->variant == TSM2X_L_OPT2;
+  if (p->tcf > 1 && !params_tsm2l) return fail(TSM2X_EINVAL, "tcf > 1 is only meaningful for the TSM2L variants");
+  return TSM2X_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// device properties
+struct DevInfo {
+  int sms = 0;
+  int major = 0, minor = 0;
+  bool ok = false;
+};
+static std::mutex g_dev_mu;
+static std::map<int, DevInfo> g_devs;
+
+static int device_info(int dev, DevInfo* out) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto it = g_devs.find(dev);
+  if (it == g_devs.end()) {
+    DevInfo d;
+    cudaDeviceProp prop;
+    cudaError_t e = cudaGetDeviceProperties(&prop, dev);
+    if (e != cudaSuccess) return fail(TSM2X_ECUDA, "cudaGetDeviceProperties(%d): %s", dev, cudaGetErrorString(e));
+    d.sms = prop.multiProcessorCount;
+    d.major = prop.major;
+    d.minor = prop.minor;
+    d.ok = (prop.major == 10 && prop.minor == 0);
+    it = g_devs.emplace(dev, d).first;
+  }
+  *out = it->second;
+  if (!out->ok)
+    return fail(TSM2X_EUNSUPPORTED, "libtsm2x.so is built for sm_100a (B200); device %d is sm_%d%d", dev, out->major,
+                out->minor);
+  return TSM2X_OK;
+}
+
+template <typename K>
+static int occupancy(K kernel, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<const void*, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = reinterpret_cast<const void*>(kernel);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem) != cudaSuccess || occ < 1) occ = 1;
+  cache[key] = occ;
+  return occ;
+}
+
+// ------------------------------------------------------------------------------------------
+// per-(device, stream) workspace: Bt + stream-K partials (grown on demand) and arrival
+// counters (zeroed on allocation, restored to zero by the kernels themselves).
+struct Workspace {
+  std::mutex mu;  // held for the whole enqueue of one call
+  void* buf = nullptr;
+  size_t cap = 0;
+  int* counters = nullptr;
+  size_t ccap = 0;
+  int* flag = nullptr;  // zero-C check result
+};
+static std::mutex g_ws_mu;
+static std::map<std::pair<int, cudaStream_t>, std::unique_ptr<Workspace>> g_ws;
+
+static Workspace* workspace_for(int dev, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  auto& slot = g_ws[{dev, s}];
+  if (!slot) slot.reset(new Workspace());
+  return slot.get();
+}
+
+static int ws_reserve(Workspace* w, size_t bytes, size_t counters, cudaStream_t s) {
+  bytes = std::max<size_t>(bytes, 1 << 20);
+  if (bytes > w->cap) {
+    if (w->buf) TSM2X_CUDA(cudaFreeAsync(w->buf, s));
+    w->buf = nullptr;
+    size_t cap = std::max(bytes, w->cap * 2);
+    if (cudaMallocAsync(&w->buf, cap, s) != cudaSuccess) {
+      cudaGetLastError();
+      w->cap = 0;
+      return fail(TSM2X_ENOMEM, "workspace allocation of %zu bytes failed", cap);
+    }
+    w->cap = cap;
+  }
+  counters = std::max<size_t>(counters + 1, 4096);
+  if (counters > w->ccap) {
+    if (w->counters) TSM2X_CUDA(cudaFreeAsync(w->counters, s));
+    w->counters = nullptr;
+    size_t cap = std::max(counters, w->ccap * 2);
+    if (cudaMallocAsync(reinterpret_cast<void**>(&w->counters), cap * sizeof(int), s) != cudaSuccess) {
+      cudaGetLastError();
+      w->ccap = 0;
+      return fail(TSM2X_ENOMEM, "counter allocation failed");
+    }
+    TSM2X_CUDA(cudaMemsetAsync(w->counters, 0, cap * sizeof(int), s));
+    w->ccap = cap;
+    w->flag = w->counters + (cap - 1);
+  }
+  return TSM2X_OK;
+}
+
+static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+static inline int nt_for(int w) { return w <= 1 ? 1 : w <= 2 ? 2 : w <= 4 ? 4 : w <= 8 ? 8 : 16; }
+static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ------------------------------------------------------------------------------------------
+
+// ---- TMA descriptor for A (2-D: dim0 = rows, dim1 = columns; OOB elements read as zero)
+static int encode_a_map(CUtensorMap* map, const void* A, int64_t m, int64_t k, int64_t lda, size_t eb, int box_rows,
+                        int box_cols) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!encode) return fail(TSM2X_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)k};
+  cuuint64_t strides[1] = {(cuuint64_t)(lda * eb)};
+  cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(map, eb == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                      const_cast<void*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TSM2X_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return TSM2X_OK;
+}
+
+// ---- paper ablation kernels (V0/V1/V2), launched with the caller's t1/t2/t3 -----------------
+template <typename T, int NT>
+static int launch_ablation_nt(int variant, int64_t m, int64_t k, int64_t n, const T* A, int64_t lda, const T* B,
+                              int64_t ldb, T* C, int64_t ldc, int t1, int t2, int t3, bool c_is_zero, cudaStream_t s) {
+  const unsigned grid = (unsigned)((m + t1 - 1) / t1);
+  if (variant == TSM2X_V1) {
+    ablation_v1<T, NT><<<grid, t1, 0, s>>>(A, lda, B, ldb, C, ldc, m, k, n, t2, c_is_zero);
+  } else {
+    const size_t smem = (size_t)t1 * NT * sizeof(T);
+    if (smem > 48 * 1024)
+      TSM2X_CUDA(cudaFuncSetAttribute(ablation_v2<T, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ablation_v2<T, NT><<<grid, t1, smem, s>>>(A, lda, B, ldb, C, ldc, m, k, n, t2, t3, c_is_zero);
+  }
+  return check_launch("ablation");
+}
+
+template <typename T>
+static int run_ablation(int variant, int64_t m, int64_t k, int64_t n, const T* A, int64_t lda, const T* B, int64_t ldb,
+                        T* C, int64_t ldc, const tsm2x_params* p, bool c_is_zero, cudaStream_t s) {
+  if (p->t1 > 1024) return fail(TSM2X_EUNSUPPORTED, "ablation kernels need t1 <= 1024 (one thread per row), got %d", p->t1);
+  if (variant == TSM2X_V0) {
+    ablation_v0<T><<<(unsigned)((m + p->t1 - 1) / p->t1), p->t1, 0, s>>>(A, lda, B, ldb, C, ldc, m, k, n, c_is_zero);
+    return check_launch("ablation_v0");
+  }
+  const int t2 = std::min(p->t2, 16);  // register width of one pass (wider t2 runs as 16-wide passes)
+  const int t3 = p->t3;
+  switch (nt_for(t2)) {
+    case 1: return launch_ablation_nt<T, 1>(variant, m, k, n, A, lda, B, ldb, C, ldc, p->t1, t2, t3, c_is_zero, s);
+    case 2: return launch_ablation_nt<T, 2>(variant, m, k, n, A, lda, B, ldb, C, ldc, p->t1, t2, t3, c_is_zero, s);
+    case 4: return launch_ablation_nt<T, 4>(variant, m, k, n, A, lda, B, ldb, C, ldc, p->t1, t2, t3, c_is_zero, s);
+    case 8: return launch_ablation_nt<T, 8>(variant, m, k, n, A, lda, B, ldb, C, ldc, p->t1, t2, t3, c_is_zero, s);
+    default: return launch_ablation_nt<T, 16>(variant, m, k, n, A, lda, B, ldb, C, ldc, p->t1, t2, t3, c_is_zero, s);
+  }
+}
+
+// ---- TSM2R pass: C[:, p:p+w] (+)= A * B[:, p:p+w] -----------------------------------------
+template <typename T, int NT>
+static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m, int64_t k, int w, const T* A,
+                          int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc, bool c_is_zero, cudaStream_t s) {
+  constexpr int THREADS = 256;
+  const bool vec = aligned16(A) && (lda % Vec<T>::N == 0);
+  const int rpt = vec ? Vec<T>::N : 1;
+  // TMA flavour needs 16B-aligned column starts (lda*eb % 16 == 0) and the vector layout
+  const bool tma_ok = vec && ((lda * (int64_t)sizeof(T)) % 16 == 0) && m < (int64_t(1) << 31) &&
+                      k < (int64_t(1) << 31);
+  if (impl == TSM2X_IMPL_AUTO) impl = tma_ok ? TSM2X_IMPL_STREAM_TMA : TSM2X_IMPL_STREAM_LDG;
+  if (impl == TSM2X_IMPL_STREAM_TMA && !tma_ok) impl = TSM2X_IMPL_STREAM_LDG;
+  const bool tma = impl == TSM2X_IMPL_STREAM_TMA;
+
+  const int R = tma ? TmaCfg<T, NT>::R : THREADS * rpt;
+  const int KC = tma ? TmaCfg<T, NT>::KC : 32;
+  const int64_t num_rb = (m + R - 1) / R;
+  const int64_t num_kb = (k + KC - 1) / KC;
+  const int64_t units = num_rb * num_kb;
+
+  StreamArgs<T> a;
+  a.A = A;
+  a.lda = lda;
+  a.C = C;
+  a.ldc = ldc;
+  a.m = m;
+  a.k = k;
+  a.w = w;
+  a.c_is_zero = c_is_zero ? 1 : 0;
+  a.num_rb = num_rb;
+  a.KC = KC;
+
+  int occ;
+  const void* kfn;
+  size_t smem = 0;
+  int threads;
+  if (tma) {
+    auto kern = tsm2r_stream_tma<T, NT>;
+    smem = TmaCfg<T, NT>::SMEM;
+    threads = TmaCfg<T, NT>::THREADS;
+    cudaError_t attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    TSM2X_CUDA(attr_err);
+    occ = occupancy(kern, threads, smem);
+    kfn = (const void*)kern;
+  } else if (vec) {
+    auto kern = tsm2r_stream_ldg<T, NT, THREADS, 8, true>;
+    threads = THREADS;
+    occ = occupancy(kern, THREADS, 0);
+    kfn = (const void*)kern;
+  } else {
+    auto kern = tsm2r_stream_ldg<T, NT, THREADS, 8, false>;
+    threads = THREADS;
+    occ = occupancy(kern, THREADS, 0);
+    kfn = (const void*)kern;
+  }
+  const int64_t G = std::min<int64_t>(units, (int64_t)di.sms * occ);
+  a.part.units = units;
+  a.part.num_kb = num_kb;
+  a.part.G = G;
+  // many-way splits (few long row blocks) are combined by a separate parallel kernel
+  const int64_t max_contrib = (num_kb * G + units - 1) / units + 1;
+  a.defer = (max_contrib > 24) ? 1 : 0;
+
+  const int64_t kpad = num_kb * KC;
+  const size_t bt_bytes = align_up((size_t)kpad * NT * sizeof(T), 256);
+  const size_t part_bytes = (size_t)G * 2 * NT * R * sizeof(T);
+  TSM2X_TRY(ws_reserve(ws, bt_bytes + part_bytes, (size_t)num_rb, s));
+  T* Bt = reinterpret_cast<T*>(ws->buf);
+  a.Bt = Bt;
+  a.ws = reinterpret_cast<T*>(static_cast<char*>(ws->buf) + bt_bytes);
+  a.counters = ws->counters;
+
+  {
+    const int64_t tot = kpad * NT;
+    const int bs = 256;
+    prep_bt<T, NT><<<(unsigned)((tot + bs - 1) / bs), bs, 0, s>>>(B, ldb, k, kpad, w, Bt);
+    TSM2X_TRY(check_launch("prep_bt"));
+  }
+  alignas(64) CUtensorMap tmap;
+  if (tma) {
+    TSM2X_TRY(encode_a_map(&tmap, A, m, k, lda, sizeof(T), TmaCfg<T, NT>::BOX, KC));
+    void* args[] = {&a, &tmap};
+    TSM2X_CUDA(cudaLaunchKernel(kfn, dim3((unsigned)G), dim3(threads), args, smem, s));
+  } else {
+    void* args[] = {&a};
+    TSM2X_CUDA(cudaLaunchKernel(kfn, dim3((unsigned)G), dim3(threads), args, smem, s));
+  }
+  TSM2X_TRY(check_launch("tsm2r_stream"));
+  if (a.defer) {
+    dim3 grid((unsigned)((R + 255) / 256), (unsigned)num_rb);
+    switch (R) {
+      case 256: reduce_partials<T, NT, 256><<<grid, 256, 0, s>>>(a); break;
+      case 512: reduce_partials<T, NT, 512><<<grid, 256, 0, s>>>(a); break;
+      case 1024: reduce_partials<T, NT, 1024><<<grid, 256, 0, s>>>(a); break;
+      default: return fail(TSM2X_EUNSUPPORTED, "no reduce kernel for R=%d", R);
+    }
+    TSM2X_TRY(check_launch("reduce_partials"));
+  }
+  return TSM2X_OK;
+}
+
+// ---- TSM2L pass ------------------------------------------------------------------------------
+template <typename T, int NT>
+static int run_tsm2l_pass(const DevInfo& di, int64_t m, int64_t k, int w, const T* A, int64_t lda, const T* B,
+                          int64_t ldb, T* C, int64_t ldc, bool c_is_zero, cudaStream_t s) {
+  constexpr int THREADS = 256;
+  constexpr int KCH = 8;
+  const bool vec = aligned16(A) && aligned16(C) && (lda % Vec<T>::N == 0) && (ldc % Vec<T>::N == 0);
+  LArgs<T> a;
+  a.A = A;
+  a.lda = lda;
+  a.B = B;
+  a.ldb = ldb;
+  a.C = C;
+  a.ldc = ldc;
+  a.m = m;
+  a.k = (int)k;
+  a.w = w;
+  a.c_is_zero = c_is_zero ? 1 : 0;
+  const int rpt = vec ? Vec<T>::N : 1;
+  const int64_t groups = (m + rpt - 1) / rpt;
+  const void* kfn;
+  int occ;
+  if (vec) {
+    auto kern = tsm2l_kernel<T, NT, THREADS, KCH, true>;
+    occ = occupancy(kern, THREADS, 0);
+    kfn = (const void*)kern;
+  } else {
+    auto kern = tsm2l_kernel<T, NT, THREADS, KCH, false>;
+    occ = occupancy(kern, THREADS, 0);
+    kfn = (const void*)kern;
+  }
+  int64_t grid = std::min<int64_t>((groups + THREADS - 1) / THREADS, (int64_t)di.sms * occ);
+  grid = std::max<int64_t>(grid, 1);
+  void* args[] = {&a};
+  TSM2X_CUDA(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(THREADS), args, 0, s));
+  return check_launch("tsm2l");
+}
+
+template <typename T>
+__global__ void nonzero_check(const T* __restrict__ C, int64_t m, int64_t n, int64_t ldc, int* flag) {
+  int64_t tot = m * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = i / m, r = i - j * m;
+    if (C[r + j * ldc] != T(0)) {
+      atomicOr(flag, 1);
+      return;
+    }
+  }
+}
+
+// ---- one full device-resident call ----------------------------------------------------------
+template <typename T>
+static int run_device(int variant, int64_t m, int64_t k, int64_t n, const T* A, int64_t lda, const T* B, int64_t ldb,
+                      T* C, int64_t ldc, const tsm2x_params* params, uint32_t flags, int impl, cudaStream_t s) {
+  int dev;
+  TSM2X_CUDA(cudaGetDevice(&dev));
+  DevInfo di;
+  TSM2X_TRY(device_info(dev, &di));
+  if (lda < m || ldb < k || ldc < m)
+    return fail(TSM2X_EINVAL, "leading dimensions too small: lda=%lld (m=%lld) ldb=%lld (k=%lld) ldc=%lld",
+                (long long)lda, (long long)m, (long long)ldb, (long long)k, (long long)ldc);
+  if (!A || !B || !C) return fail(TSM2X_EINVAL, "null matrix pointer");
+  Workspace* ws = workspace_for(dev, s);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  bool c_is_zero = (flags & TSM2X_FLAG_C_IS_ZERO) != 0;
+  if (variant == TSM2X_L_OPT2 && (flags & TSM2X_FLAG_CHECK_ZERO_C) && !c_is_zero) {
+    TSM2X_TRY(ws_reserve(ws, 0, 0, s));
+    TSM2X_CUDA(cudaMemsetAsync(ws->flag, 0, sizeof(int), s));
+    nonzero_check<T><<<di.sms * 4, 256, 0, s>>>(C, m, n, ldc, ws->flag);
+    TSM2X_TRY(check_launch("nonzero_check"));
+    int h = 0;
+    TSM2X_CUDA(cudaMemcpyAsync(&h, ws->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    TSM2X_CUDA(cudaStreamSynchronize(s));
+    if (h) return fail(TSM2X_EINVAL, "L_OPT2 stores partial sums to C and requires a zeroed C");
+    c_is_zero = true;
+  }
+  if (impl == TSM2X_IMPL_ABLATION) {
+    if (variant > TSM2X_V2) impl = TSM2X_IMPL_AUTO;
+    else return run_ablation<T>(variant, m, k, n, A, lda, B, ldb, C, ldc, params, c_is_zero, s);
+  }
+  const bool use_l = (impl == TSM2X_IMPL_TSM2L) || (impl == TSM2X_IMPL_AUTO && k <= TSM2L_KMAX);
+  if (use_l && k > TSM2L_KMAX) return fail(TSM2X_EINVAL, "TSM2L kernel needs k <= %d, got %lld", TSM2L_KMAX, (long long)k);
+  for (int64_t p = 0; p < n; p += 16) {
+    const int w = (int)std::min<int64_t>(16, n - p);
+    const int nt = nt_for(w);
+    const T* Bp = B + p * ldb;
+    T* Cp = C + p * ldc;
+    int rc;
+#define TSM2X_PASS(NTV)                                                                                     \
+  case NTV:                                                                                                 \
+    rc = use_l ? run_tsm2l_pass<T, NTV>(di, m, k, w, A, lda, Bp, ldb, Cp, ldc, c_is_zero, s)                \
+               : run_tsm2r_pass<T, NTV>(di, ws, impl, m, k, w, A, lda, Bp, ldb, Cp, ldc, c_is_zero, s);     \
+    break;
+    switch (nt) {
+      TSM2X_PASS(1)
+      TSM2X_PASS(2)
+      TSM2X_PASS(4)
+      TSM2X_PASS(8)
+      TSM2X_PASS(16)
+      default: return fail(TSM2X_EUNSUPPORTED, "bad pass width");
+    }
+#undef TSM2X_PASS
+    TSM2X_TRY(rc);
+  }
+  return TSM2X_OK;
+}
+
+static int run_device_any(int variant, int precision, int64_t m, int64_t k, int64_t n, const void* A, int64_t lda,
+                          const void* B, int64_t ldb, void* C, int64_t ldc, const tsm2x_params* p, uint32_t flags,
+                          int impl, cudaStream_t s) {
+  if (precision == TSM2X_DOUBLE)
+    return run_device<double>(variant, m, k, n, (const double*)A, lda, (const double*)B, ldb, (double*)C, ldc, p, flags,
+                              impl, s);
+  return run_device<float>(variant, m, k, n, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc, p, flags,
+                           impl, s);
+}
+
+// ------------------------------------------------------------------------------------------
+// host-buffer path: H2D of A pipelined with the kernels.
+//   TSM2R (k > TSM2L_KMAX): column slabs of A; kernel j computes C += A[:, slab j] * B[slab j, :]
+//   TSM2L: row slabs of A and C; H2D (A, C) / kernel / D2H (C) on three streams.
+struct PinnedPool {
+  std::mutex mu;
+  std::vector<std::pair<void*, size_t>> bufs;
+};
+static PinnedPool g_pinned;
+
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// parallel memcpy (pageable -> pinned staging); 2-D with pitches
+static void par_copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height) {
+  const size_t total = width * height;
+  unsigned nt = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  if (total < (8u << 20)) nt = 1;
+  auto work = [&](unsigned t) {
+    if (width == dpitch && width == spitch) {
+      size_t lo = total * t / nt, hi = total * (t + 1) / nt;
+      memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+    } else {
+      size_t lo = height * t / nt, hi = height * (t + 1) / nt;
+      for (size_t r = lo; r < hi; ++r)
+        memcpy(static_cast<char*>(dst) + r * dpitch, static_cast<const char*>(src) + r * spitch, width);
+    }
+  };
+  if (nt == 1) {
+    work(0);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < nt; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+}
+
+struct HostRun {
+  int dev = 0;
+  cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+  std::vector<void*> dev_allocs;
+  std::vector<void*> host_allocs;
+  std::vector<cudaEvent_t> events;
+  ~HostRun() {
+    if (comp) cudaStreamSynchronize(comp);
+    if (h2d) cudaStreamSynchronize(h2d);
+    if (d2h) cudaStreamSynchronize(d2h);
+    for (auto p : dev_allocs) cudaFree(p);
+    for (auto p : host_allocs) cudaFreeHost(p);
+    for (auto e : events) cudaEventDestroy(e);
+    if (h2d) cudaStreamDestroy(h2d);
+    if (comp) cudaStreamDestroy(comp);
+    if (d2h) cudaStreamDestroy(d2h);
+  }
+  int init() {
+    TSM2X_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+    TSM2X_CUDA(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking));
+    TSM2X_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+    return TSM2X_OK;
+  }
+  int dmalloc(void** p, size_t bytes) {
+    if (cudaMalloc(p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(TSM2X_ENOMEM, "device allocation of %zu bytes failed", bytes);
+    }
+    dev_allocs.push_back(*p);
+    return TSM2X_OK;
+  }
+  int hmalloc(void** p, size_t bytes) {
+    if (cudaMallocHost(p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(TSM2X_ENOMEM, "pinned allocation of %zu bytes failed", bytes);
+    }
+    host_allocs.push_back(*p);
+    return TSM2X_OK;
+  }
+  int event(cudaEvent_t* e) {
+    TSM2X_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    events.push_back(*e);
+    return TSM2X_OK;
+  }
+};
+
+// copy a 2-D host block (width bytes x height rows, host pitch) to the device, via pinned
+// staging when the source is pageable. Ordered on `st`.
+struct Stager {
+  HostRun* hr;
+  bool pinned_src;
+  std::vector<void*> stage;
+  std::vector<cudaEvent_t> done;
+  size_t stage_bytes = 0;
+  int next = 0;
+  int init(HostRun* h, bool pinned, size_t max_block, int nstage) {
+    hr = h;
+    pinned_src = pinned;
+    if (pinned) return TSM2X_OK;
+    stage_bytes = max_block;
+    stage.resize(nstage);
+    done.resize(nstage);
+    for (int i = 0; i < nstage; ++i) {
+      TSM2X_TRY(hr->hmalloc(&stage[i], stage_bytes));
+      TSM2X_TRY(hr->event(&done[i]));
+    }
+    return TSM2X_OK;
+  }
+  int copy(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height, cudaStream_t st) {
+    if (pinned_src) {
+      TSM2X_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyHostToDevice, st));
+      return TSM2X_OK;
+    }
+    int i = next;
+    next = (next + 1) % (int)stage.size();
+    TSM2X_CUDA(cudaEventSynchronize(done[i]));  // staging buffer i free again
+    par_copy2d(stage[i], width, src, spitch, width, height);
+    TSM2X_CUDA(cudaMemcpy2DAsync(dst, dpitch, stage[i], width, width, height, cudaMemcpyHostToDevice, st));
+    TSM2X_CUDA(cudaEventRecord(done[i], st));
+    return TSM2X_OK;
+  }
+};
+
+template <typename T>
+static int run_host_t(int variant, int64_t m, int64_t k, int64_t n, const T* A, int64_t lda, const T* B, int64_t ldb,
+                      const T* Cin, T* Cout, int64_t ldc, const tsm2x_params* params, uint32_t flags, int device) {
+  TSM2X_CUDA(cudaSetDevice(device));
+  DevInfo di;
+  TSM2X_TRY(device_info(device, &di));
+  if (lda < m || ldb < k || ldc < m) return fail(TSM2X_EINVAL, "leading dimensions too small");
+  bool c_is_zero = (flags & TSM2X_FLAG_C_IS_ZERO) != 0;
+  if (variant == TSM2X_L_OPT2 && !c_is_zero) {
+    // reference kernels.py:366-368: L_OPT2 requires an all-zero C (checked on the host copy)
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t i = 0; i < m; ++i)
+        if (Cin[i + j * ldc] != T(0)) return fail(TSM2X_EINVAL, "L_OPT2 stores partial sums to C and requires a zeroed C");
+    c_is_zero = true;
+  }
+  HostRun hr;
+  hr.dev = device;
+  TSM2X_TRY(hr.init());
+  const size_t eb = sizeof(T);
+  const int64_t ldd = (int64_t)align_up((size_t)m, 32);  // padded device leading dimension
+  const bool pinnedA = is_pinned(A);
+  const bool use_l = k <= TSM2L_KMAX;
+
+  // B on the device (tiny)
+  T* dB;
+  TSM2X_TRY(hr.dmalloc((void**)&dB, (size_t)k * n * eb));
+  TSM2X_CUDA(cudaMemcpy2DAsync(dB, k * eb, B, ldb * eb, k * eb, n, cudaMemcpyHostToDevice, hr.h2d));
+
+  const size_t slab_target = (size_t)256 << 20;
+  if (!use_l) {
+    // ---- TSM2R: column slabs of A, C resident on the device
+    T* dC;
+    TSM2X_TRY(hr.dmalloc((void**)&dC, (size_t)ldd * n * eb));
+    if (!c_is_zero)
+      TSM2X_CUDA(cudaMemcpy2DAsync(dC, ldd * eb, Cin, ldc * eb, m * eb, n, cudaMemcpyHostToDevice, hr.h2d));
+    int64_t sw = std::max<int64_t>(1, (int64_t)(slab_target / ((size_t)ldd * eb)));
+    sw = std::min<int64_t>(sw, k);
+    const int64_t nslab = (k + sw - 1) / sw;
+    const int nbuf = (int)std::min<int64_t>(3, nslab);
+    std::vector<T*> dA(nbuf);
+    std::vector<cudaEvent_t> loaded(nbuf), consumed(nbuf);
+    for (int i = 0; i < nbuf; ++i) {
+      TSM2X_TRY(hr.dmalloc((void**)&dA[i], (size_t)ldd * sw * eb));
+      TSM2X_TRY(hr.event(&loaded[i]));
+      TSM2X_TRY(hr.event(&consumed[i]));
+    }
+    Stager stg;
+    TSM2X_TRY(stg.init(&hr, pinnedA, (size_t)m * eb * sw, 2));
+    cudaEvent_t b_ready;
+    TSM2X_TRY(hr.event(&b_ready));
+    TSM2X_CUDA(cudaEventRecord(b_ready, hr.h2d));
+    TSM2X_CUDA(cudaStreamWaitEvent(hr.comp, b_ready, 0));
+    for (int64_t j = 0; j < nslab; ++j) {
+      const int b = (int)(j % nbuf);
+      const int64_t c0 = j * sw, cw = std::min(sw, k - c0);
+      if (j >= nbuf) TSM2X_CUDA(cudaStreamWaitEvent(hr.h2d, consumed[b], 0));
+      TSM2X_TRY(stg.copy(dA[b], ldd * eb, A + c0 * lda, lda * eb, m * eb, cw, hr.h2d));
+      TSM2X_CUDA(cudaEventRecord(loaded[b], hr.h2d));
+      TSM2X_CUDA(cudaStreamWaitEvent(hr.comp, loaded[b], 0));
+      uint32_t f = (c_is_zero && j == 0) ? TSM2X_FLAG_C_IS_ZERO : 0;
+      TSM2X_TRY(run_device<T>(variant == TSM2X_L_OPT2 ? TSM2X_L_OPT1 : variant, m, cw, n, dA[b], ldd, dB + c0, k, dC,
+                              ldd, params, f, TSM2X_IMPL_AUTO, hr.comp));
+      TSM2X_CUDA(cudaEventRecord(consumed[b], hr.comp));
+    }
+    TSM2X_CUDA(cudaMemcpy2DAsync(Cout, ldc * eb, dC, ldd * eb, m * eb, n, cudaMemcpyDeviceToHost, hr.comp));
+    TSM2X_CUDA(cudaStreamSynchronize(hr.comp));
+    return TSM2X_OK;
+  }
+
+  // ---- TSM2L: row slabs of A and C
+  const size_t row_bytes = (size_t)(k + (c_is_zero ? 0 : n)) * eb;
+  int64_t rs = std::max<int64_t>(1024, (int64_t)(slab_target / std::max<size_t>(row_bytes, 1)));
+  rs = (int64_t)align_up((size_t)std::min<int64_t>(rs, m), 32);
+  const int64_t nslab = (m + rs - 1) / rs;
+  const int nbuf = (int)std::min<int64_t>(3, nslab);
+  std::vector<T*> dA(nbuf), dC(nbuf);
+  std::vector<cudaEvent_t> loaded(nbuf), computed(nbuf), drained(nbuf);
+  for (int i = 0; i < nbuf; ++i) {
+    TSM2X_TRY(hr.dmalloc((void**)&dA[i], (size_t)rs * k * eb));
+    TSM2X_TRY(hr.dmalloc((void**)&dC[i], (size_t)rs * n * eb));
+    TSM2X_TRY(hr.event(&loaded[i]));
+    TSM2X_TRY(hr.event(&computed[i]));
+    TSM2X_TRY(hr.event(&drained[i]));
+  }
+  Stager stg;
+  TSM2X_TRY(stg.init(&hr, pinnedA && (c_is_zero || is_pinned(Cin)), (size_t)rs * std::max<int64_t>(k, n) * eb, 2));
+  const bool pinnedOut = is_pinned(Cout);
+  T* out_stage[2] = {nullptr, nullptr};
+  cudaEvent_t out_done[2];
+  if (!pinnedOut) {
+    for (int i = 0; i < 2; ++i) {
+      TSM2X_TRY(hr.hmalloc((void**)&out_stage[i], (size_t)rs * n * eb));
+      TSM2X_TRY(hr.event(&out_done[i]));
+    }
+  }
+  cudaEvent_t b_ready;
+  TSM2X_TRY(hr.event(&b_ready));
+  TSM2X_CUDA(cudaEventRecord(b_ready, hr.h2d));
+  TSM2X_CUDA(cudaStreamWaitEvent(hr.comp, b_ready, 0));
+  // pageable output: slab j's staged result is copied out once slab j+1 is enqueued
+  int64_t pend_r0 = -1, pend_rw = 0;
+  int pend_i = 0;
+  auto flush_out = [&](void) -> int {
+    if (pend_r0 < 0) return TSM2X_OK;
+    TSM2X_CUDA(cudaEventSynchronize(out_done[pend_i]));
+    par_copy2d(Cout + pend_r0, ldc * eb, out_stage[pend_i], pend_rw * eb, pend_rw * eb, n);
+    pend_r0 = -1;
+    return TSM2X_OK;
+  };
+  for (int64_t j = 0; j < nslab; ++j) {
+    const int b = (int)(j % nbuf);
+    const int64_t r0 = j * rs, rw = std::min(rs, m - r0);
+    if (j >= nbuf) TSM2X_CUDA(cudaStreamWaitEvent(hr.h2d, drained[b], 0));
+    TSM2X_TRY(stg.copy(dA[b], rs * eb, A + r0, lda * eb, rw * eb, k, hr.h2d));
+    if (!c_is_zero) TSM2X_TRY(stg.copy(dC[b], rs * eb, Cin + r0, ldc * eb, rw * eb, n, hr.h2d));
+    TSM2X_CUDA(cudaEventRecord(loaded[b], hr.h2d));
+    TSM2X_CUDA(cudaStreamWaitEvent(hr.comp, loaded[b], 0));
+    TSM2X_TRY(run_device<T>(TSM2X_L_OPT1, rw, k, n, dA[b], rs, dB, k, dC[b], rs, params,
+                            c_is_zero ? TSM2X_FLAG_C_IS_ZERO : 0, TSM2X_IMPL_AUTO, hr.comp));
+    TSM2X_CUDA(cudaEventRecord(computed[b], hr.comp));
+    TSM2X_CUDA(cudaStreamWaitEvent(hr.d2h, computed[b], 0));
+    if (pinnedOut) {
+      TSM2X_CUDA(cudaMemcpy2DAsync(Cout + r0, ldc * eb, dC[b], rs * eb, rw * eb, n, cudaMemcpyDeviceToHost, hr.d2h));
+      TSM2X_CUDA(cudaEventRecord(drained[b], hr.d2h));
+    } else {
+      const int oi = (int)(j % 2);
+      if (pend_r0 >= 0 && pend_i == oi) TSM2X_TRY(flush_out());
+      TSM2X_CUDA(cudaMemcpy2DAsync(out_stage[oi], rw * eb, dC[b], rs * eb, rw * eb, n, cudaMemcpyDeviceToHost, hr.d2h));
+      TSM2X_CUDA(cudaEventRecord(drained[b], hr.d2h));
+      TSM2X_CUDA(cudaEventRecord(out_done[oi], hr.d2h));
+      TSM2X_TRY(flush_out());
+      pend_r0 = r0;
+      pend_rw = rw;
+      pend_i = oi;
+    }
+  }
+  TSM2X_TRY(flush_out());
+  TSM2X_CUDA(cudaStreamSynchronize(hr.d2h));
+  TSM2X_CUDA(cudaStreamSynchronize(hr.comp));
+  return TSM2X_OK;
+}
+
+// counter-based uniform generator (see tsm2x.h tsm2x_fill_uniform)
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+template <typename T>
+__global__ void fill_uniform(T* p, int64_t rows, int64_t cols, int64_t ld, int64_t r0, int64_t c0, uint64_t seed) {
+  const int64_t tot = rows * cols;
+  const uint64_t base = seed * 0x9E3779B97F4A7C15ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = i / rows, r = i - j * rows;
+    const uint64_t key = ((uint64_t)(c0 + j) << 32) | (uint64_t)(r0 + r);
+    const double u = (double)(splitmix64(base + key) >> 11) * 0x1.0p-53;
+    p[r + j * ld] = (T)u;
+  }
+}
+
+}  // namespace tsm2x
+
+// ============================================================================================
+// C ABI
+using namespace tsm2x;
+
+extern "C" {
+
+int tsm2x_validate(int variant, int64_t m, int64_t k, int64_t n, const tsm2x_params* params) {
+  return validate(variant, TSM2X_DOUBLE, m, k, n, params);
+}
+
+int tsm2x_run_ex(int variant, int precision, int64_t m, int64_t k, int64_t n, const void* A, int64_t lda,
+                 const void* B, int64_t ldb, void* C, int64_t ldc, const tsm2x_params* params, uint32_t flags,
+                 int impl, void* stream) {
+  TSM2X_TRY(validate(variant, precision, m, k, n, params));
+  if (impl < TSM2X_IMPL_AUTO || impl > TSM2X_IMPL_ABLATION) return fail(TSM2X_EINVAL, "unknown impl %d", impl);
+  return run_device_any(variant, precision, m, k, n, A, lda, B, ldb, C, ldc, params, flags, impl,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+int tsm2x_run(int variant, int precision, int64_t m, int64_t k, int64_t n, const void* A, int64_t lda, const void* B,
+              int64_t ldb, void* C, int64_t ldc, const tsm2x_params* params, uint32_t flags, void* stream) {
+  return tsm2x_run_ex(variant, precision, m, k, n, A, lda, B, ldb, C, ldc, params, flags, TSM2X_IMPL_AUTO, stream);
+}
+
+int tsm2x_run_host(int variant, int precision, int64_t m, int64_t k, int64_t n, const void* A, int64_t lda,
+                   const void* B, int64_t ldb, const void* C_in, void* C_out, int64_t ldc,
+                   const tsm2x_params* params, uint32_t flags, int device) {
+  TSM2X_TRY(validate(variant, precision, m, k, n, params));
+  if (!A || !B || !C_out || (!C_in && !(flags & TSM2X_FLAG_C_IS_ZERO))) return fail(TSM2X_EINVAL, "null host pointer");
+  if (precision == TSM2X_DOUBLE)
+    return run_host_t<double>(variant, m, k, n, (const double*)A, lda, (const double*)B, ldb, (const double*)C_in,
+                              (double*)C_out, ldc, params, flags, device);
+  return run_host_t<float>(variant, m, k, n, (const float*)A, lda, (const float*)B, ldb, (const float*)C_in,
+                           (float*)C_out, ldc, params, flags, device);
+}
+
+int tsm2x_fill_uniform(int precision, int64_t rows, int64_t cols, void* ptr, int64_t ld, int64_t row_offset,
+                       int64_t col_offset, uint64_t seed, void* stream) {
+  if (rows < 1 || cols < 1 || ld < rows || !ptr || row_offset < 0 || col_offset < 0 ||
+      row_offset + rows > (int64_t(1) << 32))
+    return fail(TSM2X_EINVAL, "bad fill_uniform arguments");
+  int dev;
+  TSM2X_CUDA(cudaGetDevice(&dev));
+  DevInfo di;
+  TSM2X_TRY(device_info(dev, &di));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned grid = (unsigned)std::min<int64_t>((rows * cols + 255) / 256, (int64_t)di.sms * 16);
+  if (precision == TSM2X_DOUBLE)
+    fill_uniform<double><<<grid, 256, 0, s>>>((double*)ptr, rows, cols, ld, row_offset, col_offset, seed);
+  else
+    fill_uniform<float><<<grid, 256, 0, s>>>((float*)ptr, rows, cols, ld, row_offset, col_offset, seed);
+  return check_launch("fill_uniform");
+}
+
+const char* tsm2x_last_error(void) { return t_err.c_str(); }
+int tsm2x_version(void) { return 100; }
+const char* tsm2x_build_target(void) { return "sm_100a"; }
+int64_t tsm2x_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

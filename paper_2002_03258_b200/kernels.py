@@ -1,0 +1,147 @@
+"""The drop-in entry points.
+
+* :func:`run_native` — same signature, argument conventions and errors as the reference
+  ``tsgemm.kernels.run_native(variant, A, B, C, params) -> Matrix`` (kernels.py:391-416):
+  returns a NEW frozen Matrix holding ``C + A @ B`` (the caller's C is never mutated); L_OPT2
+  requires an all-zero C (kernels.py:366-368). Host matrices go through ``tsm2x_run_host``,
+  which pipelines the H2D copy of A with the sm_100a kernels.
+* :func:`gemm` — the device-resident form on column-major torch CUDA tensors
+  (``tsm2x_run``), stream-ordered, for callers that keep A in HBM (the benchmark, the
+  multi-GPU driver, k-means / ABFT consumers named in PAPER.md:55-56).
+* :func:`simulate` — the reference's SIMT-simulator entry point has no GPU meaning; it raises
+  NotImplementedError pointing at ncu (out of scope).
+
+Results never depend on ``params`` (reference README.md:88-92); the production kernels take
+their tiling from :mod:`paper_2002_03258_b200.tuning`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .core import Matrix, Precision, Variant, check_dims, validate_params_for
+
+
+def _params_struct(params) -> _lib.Params:
+    v = Variant.coerce(getattr(params, "variant", Variant.V3))
+    return _lib.Params(int(params.t1), int(params.t2), int(params.t3), int(params.tcf), v.ordinal)
+
+
+def _flat(M, dtype) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(M.storage).reshape(-1))
+    if a.dtype != dtype:
+        a = a.astype(dtype)
+    return a
+
+
+def run_native(variant, A, B, C, params) -> Matrix:
+    """``C + A @ B`` on the B200 for column-major Matrix inputs (reference kernels.py:391-416)."""
+    variant = Variant.coerce(variant)
+    m, k, n = check_dims(A, B, C)
+    validate_params_for(params, m, k, n)
+    prec = Precision.coerce(A.precision)
+    dtype = prec.dtype
+    a, b, c = _flat(A, dtype), _flat(B, dtype), _flat(C, dtype)
+    flags = 0
+    if variant is Variant.L_OPT2:
+        if np.any(c != 0):
+            raise ValueError("L_OPT2 stores partial sums to C and requires a zeroed C")
+        flags |= _lib.FLAG_C_IS_ZERO
+    out = np.empty(m * n, dtype=dtype)
+    lib = _lib.load()
+    p = _params_struct(params)
+    rc = lib.tsm2x_run_host(
+        variant.ordinal, _lib.DOUBLE if prec is Precision.DOUBLE else _lib.SINGLE, m, k, n,
+        a.ctypes.data, m, b.ctypes.data, k, c.ctypes.data, out.ctypes.data, m, ctypes.byref(p), flags,
+        _current_device())
+    _lib.check(rc)
+    return Matrix._adopt(m, n, out, prec)
+
+
+def simulate(*args, **kwargs):
+    raise NotImplementedError(
+        "simulate() is the reference's CPU SIMT model (kernels.py:371-388); on B200 the real kernels run "
+        "via run_native/gemm and Nsight Compute supplies the counters (see DESIGN.md)")
+
+
+def _current_device() -> int:
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except Exception:  # pragma: no cover - torch absent
+        pass
+    return 0
+
+
+# ---------------------------------------------------------------------------------------------
+# device-resident API (torch tensors)
+
+def colmajor_empty(rows: int, cols: int, dtype, device, pad_to: int = 32):
+    """An uninitialised (rows x cols) column-major CUDA tensor whose leading dimension is
+    padded to a multiple of ``pad_to`` elements (keeps every column 16-B aligned for TMA)."""
+    import torch
+    ld = (rows + pad_to - 1) // pad_to * pad_to
+    base = torch.empty((cols, ld), dtype=dtype, device=device)
+    return base.t()[:rows, :]
+
+
+def _ld(t, rows: int) -> int:
+    if t.dim() != 2:
+        raise ValueError("expected a 2-D tensor")
+    s0, s1 = t.stride()
+    if s0 != 1 and not (t.shape[0] == 1):
+        raise ValueError("tensor must be column-major (stride(0) == 1); use colmajor_empty or x.t().contiguous().t()")
+    ld = s1 if t.shape[1] > 1 else max(s1, rows)
+    return max(int(ld), rows)
+
+
+def gemm(A, B, C, *, variant=Variant.V3, params=None, c_is_zero: bool = False, impl: str = "auto",
+         stream=None, check_zero_c: bool = False):
+    """In place on device: ``C (+)= A @ B`` for column-major CUDA tensors (fp32 or fp64).
+
+    ``c_is_zero`` elides the read of C (the L_OPT2 contract). Stream-ordered on ``stream``
+    (default: torch's current stream); returns C.
+    """
+    import torch
+    from .core import KernelParams
+    variant = Variant.coerce(variant)
+    if not (A.is_cuda and B.is_cuda and C.is_cuda):
+        raise ValueError("gemm expects CUDA tensors; use run_native for host matrices")
+    if not (A.dtype == B.dtype == C.dtype) or A.dtype not in (torch.float32, torch.float64):
+        raise ValueError("A, B, C must share one precision (float32 or float64)")
+    m, k = A.shape
+    if B.shape[0] != k or C.shape[0] != m or B.shape[1] != C.shape[1]:
+        raise ValueError(f"dimension mismatch: A {m}x{k}, B {B.shape[0]}x{B.shape[1]}, C {C.shape[0]}x{C.shape[1]}")
+    n = B.shape[1]
+    if params is None:
+        params = KernelParams(t1=128, t2=min(4, n), t3=4, tcf=1, variant=variant)
+    validate_params_for(params, m, k, n)
+    prec = _lib.DOUBLE if A.dtype == torch.float64 else _lib.SINGLE
+    flags = (_lib.FLAG_C_IS_ZERO if c_is_zero else 0) | (_lib.FLAG_CHECK_ZERO_C if check_zero_c else 0)
+    if stream is None:
+        stream = torch.cuda.current_stream(A.device)
+    p = _params_struct(params)
+    with torch.cuda.device(A.device):
+        rc = _lib.load().tsm2x_run_ex(
+            variant.ordinal, prec, m, k, n, A.data_ptr(), _ld(A, m), B.data_ptr(), _ld(B, k), C.data_ptr(),
+            _ld(C, m), ctypes.byref(p), flags, _lib.IMPL[impl], ctypes.c_void_p(stream.cuda_stream))
+    _lib.check(rc)
+    return C
+
+
+def fill_uniform(T, seed: int, row_offset: int = 0, col_offset: int = 0, stream=None):
+    """Fills a column-major CUDA tensor with the counter-based U[0,1) generator (tsm2x.h)."""
+    import torch
+    rows, cols = T.shape
+    prec = _lib.DOUBLE if T.dtype == torch.float64 else _lib.SINGLE
+    if stream is None:
+        stream = torch.cuda.current_stream(T.device)
+    with torch.cuda.device(T.device):
+        rc = _lib.load().tsm2x_fill_uniform(prec, rows, cols, T.data_ptr(), _ld(T, rows), row_offset, col_offset,
+                                            seed & 0xFFFFFFFFFFFFFFFF, ctypes.c_void_p(stream.cuda_stream))
+    _lib.check(rc)
+    return T

@@ -1,0 +1,268 @@
+"""GPU parity: the sm_100a kernels against the CPU oracle (oracle/reference.py, itself pinned to
+the reference package by tests/test_oracle_golden.py).
+
+Tolerances (BASELINE.json north_star): relative Frobenius error <= 1e-12 (fp64), <= 1e-5 (fp32);
+plus the reference's own acceptance bound max_rel_error <= 8*k*eps (test_acceptance.py:72-74).
+Exact cases (identity, zero B, small integers) must be bitwise.
+"""
+
+import zlib
+
+import numpy as np
+import pytest
+
+from conftest import TOL_FROB, golden_cases, regenerate
+from oracle import max_rel_error, naive_gemm, rel_frobenius
+
+pytestmark = pytest.mark.gpu
+
+EXACT = {"identity_v3", "zero_b_v0", "scalar_fma", "single_accumulates_double"}
+
+
+def _tsm():
+    import paper_2002_03258_b200 as tsm
+    return tsm
+
+
+def _mat(tsm, X, prec):
+    return tsm.Matrix(X.shape[0], X.shape[1], X.reshape(-1, order="F"), prec)
+
+
+def _check(out2d, ref2d, k, precision, exact=False, what=""):
+    if exact:
+        assert np.array_equal(out2d, ref2d), what
+        return
+    eps = np.finfo(np.float64 if precision == "double" else np.float32).eps
+    fro = rel_frobenius(out2d, ref2d)
+    mre = max_rel_error(out2d, ref2d)
+    assert fro <= TOL_FROB[precision], (what, fro)
+    assert mre <= 8 * k * eps, (what, mre)
+
+
+@pytest.mark.parametrize("case", golden_cases(), ids=lambda c: c["name"])
+def test_run_native_golden(case):
+    """Every golden case through the drop-in run_native (host Matrix in/out)."""
+    tsm = _tsm()
+    A, B, C0 = regenerate(case)
+    prec = tsm.Precision.parse(case["precision"])
+    p = case["params"]
+    variant = tsm.Variant.parse(case["variant"])
+    params = tsm.KernelParams(t1=p["t1"], t2=p["t2"], t3=p["t3"], tcf=p["tcf"], variant=variant)
+    out = tsm.run_native(variant, _mat(tsm, A, prec), _mat(tsm, B, prec), _mat(tsm, C0, prec), params)
+    assert isinstance(out, tsm.Matrix) and out.rows == case["m"] and out.cols == case["n"]
+    assert not out.storage.flags.writeable
+    ref = naive_gemm(A, B, C0)
+    _check(out.to_2d(), ref, case["k"], case["precision"], exact=case["name"] in EXACT, what=case["name"])
+
+
+@pytest.mark.parametrize("impl", ["auto", "ldg", "tma", "tsm2l", "ablation"])
+@pytest.mark.parametrize("variant", ["v0", "v1", "v2", "v3", "l-opt1", "l-opt2"])
+def test_device_impls_ragged(impl, variant):
+    """Device API, every implementation x variant, ragged shapes, odd leading dimensions."""
+    import torch
+    tsm = _tsm()
+    rng = np.random.default_rng(zlib.crc32(f"{impl}/{variant}".encode()))
+    for (m, k, n) in [(1, 1, 1), (37, 5, 3), (333, 61, 7), (1025, 257, 16), (700, 1999, 9), (4099, 64, 2)]:
+        if impl == "tsm2l" and k > 64:
+            continue
+        for dtype in (np.float64, np.float32):
+            A = rng.random((m, k)).astype(dtype)
+            B = rng.random((k, n)).astype(dtype)
+            C0 = np.zeros((m, n), dtype) if variant == "l-opt2" else rng.random((m, n)).astype(dtype)
+            dev = torch.device("cuda")
+            # odd leading dimension on purpose: exercises the scalar / LDG paths
+            lda = m + (1 if m % 2 else 3)
+            At = torch.zeros((k, lda), dtype=torch.from_numpy(A).dtype, device=dev).t()[:m]
+            At.copy_(torch.from_numpy(A))
+            Bt = torch.from_numpy(np.asfortranarray(B)).to(dev).t().contiguous().t()
+            Ct = torch.from_numpy(np.asfortranarray(C0)).to(dev).t().contiguous().t()
+            tsm.gemm(At, Bt, Ct, variant=variant, impl=impl, c_is_zero=(variant == "l-opt2"),
+                     params=tsm.KernelParams(t1=64, t2=1, t3=4, tcf=1, variant=tsm.Variant.parse(variant)))
+            torch.cuda.synchronize()
+            prec = "double" if dtype == np.float64 else "single"
+            _check(Ct.cpu().numpy(), naive_gemm(A, B, C0), k, prec, what=(impl, variant, m, k, n, prec))
+
+
+def test_aligned_tma_many_shapes():
+    """The TMA path on padded (aligned) layouts, covering k tails, row tails and stream-K splits."""
+    import torch
+    tsm = _tsm()
+    rng = np.random.default_rng(7)
+    shapes = [(512, 8, 4), (513, 9, 4), (4096, 4096, 8), (1000, 3001, 16), (64, 20000, 2), (5000, 100, 1),
+              (2049, 777, 12), (30, 65, 16)]
+    for (m, k, n) in shapes:
+        for dt in (torch.float64, torch.float32):
+            A = tsm.colmajor_empty(m, k, dt, "cuda")
+            A.copy_(torch.from_numpy(rng.random((m, k))).to(dt))
+            B = tsm.colmajor_empty(k, n, dt, "cuda")
+            B.copy_(torch.from_numpy(rng.random((k, n))).to(dt))
+            C = tsm.colmajor_empty(m, n, dt, "cuda")
+            C0 = rng.random((m, n))
+            C.copy_(torch.from_numpy(C0).to(dt))
+            tsm.gemm(A, B, C, impl="tma")
+            torch.cuda.synchronize()
+            An, Bn = A.cpu().numpy(), B.cpu().numpy()
+            ref = naive_gemm(An, Bn, C0.astype(An.dtype))
+            _check(C.cpu().numpy(), ref, k, "double" if dt == torch.float64 else "single", what=(m, k, n, dt))
+
+
+def test_deterministic_repeat():
+    """Fixed-order stream-K combine: two launches give bitwise-identical C."""
+    import torch
+    tsm = _tsm()
+    m, k, n = 6000, 20000, 8
+    A = tsm.colmajor_empty(m, k, torch.float64, "cuda")
+    tsm.fill_uniform(A, seed=11)
+    B = tsm.colmajor_empty(k, n, torch.float64, "cuda")
+    tsm.fill_uniform(B, seed=12)
+    outs = []
+    for _ in range(3):
+        C = tsm.colmajor_empty(m, n, torch.float64, "cuda")
+        C.zero_()
+        tsm.gemm(A, B, C, c_is_zero=True)
+        outs.append(C.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+def test_fill_uniform_matches_host_rng():
+    import torch
+    from oracle.rng import uniform_block
+    tsm = _tsm()
+    for dt, npdt in ((torch.float64, np.float64), (torch.float32, np.float32)):
+        T = tsm.colmajor_empty(300, 7, dt, "cuda")
+        tsm.fill_uniform(T, seed=2024, row_offset=1000, col_offset=5)
+        host = uniform_block(range(1000, 1300), range(5, 12), 2024, npdt)
+        assert np.array_equal(T.cpu().numpy(), host)
+
+
+def test_l_opt2_nonzero_c_rejected():
+    tsm = _tsm()
+    A = tsm.Matrix.from_2d(np.ones((256, 8)), tsm.Precision.DOUBLE)
+    B = tsm.Matrix.from_2d(np.ones((8, 8)), tsm.Precision.DOUBLE)
+    C = tsm.Matrix.from_2d(np.ones((256, 8)), tsm.Precision.DOUBLE)
+    p = tsm.KernelParams(t1=32, t2=8, t3=4, tcf=2, variant=tsm.Variant.L_OPT2)
+    with pytest.raises(ValueError):
+        tsm.run_native(tsm.Variant.L_OPT2, A, B, C, p)
+
+
+def test_l_opt2_device_check():
+    import torch
+    tsm = _tsm()
+    A = torch.ones((64, 4), dtype=torch.float64, device="cuda").t().contiguous().t()
+    B = torch.ones((4, 4), dtype=torch.float64, device="cuda")
+    C = torch.ones((64, 4), dtype=torch.float64, device="cuda").t().contiguous().t()
+    with pytest.raises(ValueError):
+        tsm.gemm(A, B, C, variant="l-opt2", check_zero_c=True)
+    C.zero_()
+    tsm.gemm(A, B, C, variant="l-opt2", check_zero_c=True)
+    assert torch.all(C == 4.0)
+
+
+def test_wide_n_multi_pass():
+    """n > 16 runs as 16-wide passes (A re-read per pass, as the paper's t2 passes)."""
+    tsm = _tsm()
+    rng = np.random.default_rng(3)
+    for (m, k, n) in [(700, 300, 40), (3000, 40, 33)]:
+        A, B, C0 = rng.random((m, k)), rng.random((k, n)), rng.random((m, n))
+        out = tsm.run_native(tsm.Variant.V3, tsm.Matrix.from_2d(A, "double"), tsm.Matrix.from_2d(B, "double"),
+                             tsm.Matrix.from_2d(C0, "double"), tsm.KernelParams(t2=4))
+        _check(out.to_2d(), naive_gemm(A, B, C0), k, "double")
+
+
+def test_host_path_pinned_and_pageable_slabs():
+    """run_host with several H2D slabs (TSM2R column slabs, TSM2L row slabs), pinned and pageable."""
+    import ctypes
+    import torch
+    from paper_2002_03258_b200 import _lib
+    rng = np.random.default_rng(4)
+    for (m, k, n) in [(8192, 9000, 8), (3_000_000, 16, 16)]:
+        A = np.asfortranarray(rng.random((m, k)))
+        B = np.asfortranarray(rng.random((k, n)))
+        C0 = np.asfortranarray(rng.random((m, n)))
+        for pinned in (False, True):
+            if pinned:
+                At = torch.from_numpy(A.T.copy()).pin_memory()  # (k, m) row-major == A column-major
+                a_ptr = At.data_ptr()
+            else:
+                a_ptr = A.ctypes.data
+            out = np.empty((m, n), order="F")
+            p = _lib.Params(128, 4, 4, 1, 3)
+            rc = _lib.load().tsm2x_run_host(3, _lib.DOUBLE, m, k, n, a_ptr, m, B.ctypes.data, k, C0.ctypes.data,
+                                            out.ctypes.data, m, ctypes.byref(p), 0, 0)
+            _lib.check(rc)
+            rows = np.r_[0:64, m // 2:m // 2 + 64, m - 64:m]
+            ref = naive_gemm(A[rows], B, C0[rows])
+            _check(out[rows], ref, k, "double", what=(m, k, n, pinned))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n", [2, 4, 8, 16])
+def test_config2_sampled_rows(n):
+    """BASELINE config 2 (ref m=k=30720, n=2..16, fp64) at full size: sampled row slabs against
+    the oracle (rows are independent, so slabs are exact restrictions) and the full result
+    against cuBLAS DGEMM (relative Frobenius)."""
+    import torch
+    from oracle.rng import uniform_block
+    tsm = _tsm()
+    m = k = 30720
+    A = tsm.colmajor_empty(m, k, torch.float64, "cuda")
+    tsm.fill_uniform(A, seed=2024)
+    B = tsm.colmajor_empty(k, n, torch.float64, "cuda")
+    tsm.fill_uniform(B, seed=2025)
+    C = tsm.colmajor_empty(m, n, torch.float64, "cuda")
+    C.zero_()
+    tsm.gemm(A, B, C, c_is_zero=True)
+    torch.cuda.synchronize()
+    Bh = uniform_block(range(k), range(n), 2025)
+    Ch = C.cpu().numpy()
+    for r0 in (0, 12345, m - 256):
+        rows = range(r0, r0 + 256)
+        Ah = uniform_block(rows, range(k), 2024)
+        ref = naive_gemm(Ah, Bh, np.zeros((256, n)))
+        _check(Ch[r0:r0 + 256], ref, k, "double", what=("slab", r0))
+    full = (A @ B).cpu().numpy()
+    assert rel_frobenius(Ch, full) <= 1e-12
+
+
+@pytest.mark.slow
+def test_config3_tsm2l_sampled():
+    import torch
+    from oracle.rng import uniform_block
+    tsm = _tsm()
+    m, k, n = 1 << 24, 16, 16
+    A = tsm.colmajor_empty(m, k, torch.float64, "cuda")
+    tsm.fill_uniform(A, seed=7)
+    B = tsm.colmajor_empty(k, n, torch.float64, "cuda")
+    tsm.fill_uniform(B, seed=8)
+    C = tsm.colmajor_empty(m, n, torch.float64, "cuda")
+    tsm.fill_uniform(C, seed=9)
+    tsm.gemm(A, B, C, variant="l-opt1")
+    torch.cuda.synchronize()
+    Bh = uniform_block(range(k), range(n), 8)
+    for r0 in (0, m // 3, m - 1000):
+        rows = range(r0, r0 + 1000)
+        ref = naive_gemm(uniform_block(rows, range(k), 7), Bh, uniform_block(rows, range(n), 9))
+        _check(C[r0:r0 + 1000].cpu().numpy(), ref, k, "double", what=r0)
+
+
+@pytest.mark.slow
+def test_config4_fp32_sampled():
+    import torch
+    from oracle.rng import uniform_block
+    tsm = _tsm()
+    m = k = 32768
+    n = 16
+    A = tsm.colmajor_empty(m, k, torch.float32, "cuda")
+    tsm.fill_uniform(A, seed=31)
+    B = tsm.colmajor_empty(k, n, torch.float32, "cuda")
+    tsm.fill_uniform(B, seed=32)
+    C = tsm.colmajor_empty(m, n, torch.float32, "cuda")
+    C.zero_()
+    tsm.gemm(A, B, C, c_is_zero=True)
+    torch.cuda.synchronize()
+    Ch = C.cpu().numpy()
+    Bh = uniform_block(range(k), range(n), 32, np.float32)
+    for r0 in (0, m - 128):
+        rows = range(r0, r0 + 128)
+        ref = naive_gemm(uniform_block(rows, range(k), 31, np.float32), Bh, np.zeros((128, n), np.float32))
+        _check(Ch[r0:r0 + 128], ref, k, "single", what=r0)
