@@ -106,6 +106,11 @@ int tsm2x_run_host(int variant, int precision, int64_t m, int64_t k, int64_t n,
 int tsm2x_fill_uniform(int precision, int64_t rows, int64_t cols, void* ptr, int64_t ld, int64_t row_offset,
                        int64_t col_offset, uint64_t seed, void* stream);
 
+/* Profiling hook (bench evidence): the NEXT main kernel launched by this thread (the TSM2R
+ * stream kernel or the TSM2L kernel of the next run call) is bracketed by cudaEventRecord of
+ * these two cudaEvent_t on its stream; the hook then clears. Pass NULLs to clear explicitly. */
+int tsm2x_set_kernel_events(void* start_event, void* stop_event);
+
 /* Thread-local message describing the last non-OK return on this thread. */
 const char* tsm2x_last_error(void);
 

@@ -28,6 +28,7 @@ EXPORTS = (
     "tsm2x_version",
     "tsm2x_build_target",
     "tsm2x_launch_count",
+    "tsm2x_set_kernel_events",
 )
 
 
@@ -61,8 +62,9 @@ def load() -> ctypes.CDLL:
         lib.tsm2x_run_ex.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, pp, u32, i32, vp]
         lib.tsm2x_run_host.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, vp, i64, pp, u32, i32]
         lib.tsm2x_fill_uniform.argtypes = [i32, i64, i64, vp, i64, i64, i64, ctypes.c_uint64, vp]
+        lib.tsm2x_set_kernel_events.argtypes = [vp, vp]
         for name in ("tsm2x_validate", "tsm2x_run", "tsm2x_run_ex", "tsm2x_run_host", "tsm2x_fill_uniform",
-                     "tsm2x_version"):
+                     "tsm2x_version", "tsm2x_set_kernel_events"):
             getattr(lib, name).restype = ctypes.c_int
         lib.tsm2x_last_error.restype = ctypes.c_char_p
         lib.tsm2x_build_target.restype = ctypes.c_char_p

@@ -28,6 +28,7 @@ namespace tsm2x {
 // ------------------------------------------------------------------------------------------
 // errors
 static thread_local std::string t_err;
+static thread_local cudaEvent_t t_ev_start = nullptr, t_ev_stop = nullptr;
 static std::atomic<int64_t> g_launches{0};
 
 static int fail(int code, const char* fmt, ...) {
@@ -321,6 +322,8 @@ static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m,
     TSM2X_TRY(check_launch("prep_bt"));
   }
   alignas(64) CUtensorMap tmap;
+  const bool timed = t_ev_start && t_ev_stop;
+  if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
   if (tma) {
     TSM2X_TRY(encode_a_map(&tmap, A, m, k, lda, sizeof(T), TmaCfg<T, NT>::BOX, KC));
     void* args[] = {&a, &tmap};
@@ -330,6 +333,10 @@ static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m,
     TSM2X_CUDA(cudaLaunchKernel(kfn, dim3((unsigned)G), dim3(threads), args, smem, s));
   }
   TSM2X_TRY(check_launch("tsm2r_stream"));
+  if (timed) {
+    TSM2X_CUDA(cudaEventRecord(t_ev_stop, s));
+    t_ev_start = t_ev_stop = nullptr;
+  }
   if (a.defer) {
     dim3 grid((unsigned)((R + 255) / 256), (unsigned)num_rb);
     switch (R) {
@@ -377,8 +384,15 @@ static int run_tsm2l_pass(const DevInfo& di, int64_t m, int64_t k, int w, const 
   int64_t grid = std::min<int64_t>((groups + THREADS - 1) / THREADS, (int64_t)di.sms * occ);
   grid = std::max<int64_t>(grid, 1);
   void* args[] = {&a};
+  const bool timed = t_ev_start && t_ev_stop;
+  if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
   TSM2X_CUDA(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(THREADS), args, 0, s));
-  return check_launch("tsm2l");
+  TSM2X_TRY(check_launch("tsm2l"));
+  if (timed) {
+    TSM2X_CUDA(cudaEventRecord(t_ev_stop, s));
+    t_ev_start = t_ev_stop = nullptr;
+  }
+  return TSM2X_OK;
 }
 
 template <typename T>
@@ -802,6 +816,12 @@ int tsm2x_fill_uniform(int precision, int64_t rows, int64_t cols, void* ptr, int
   else
     fill_uniform<float><<<grid, 256, 0, s>>>((float*)ptr, rows, cols, ld, row_offset, col_offset, seed);
   return check_launch("fill_uniform");
+}
+
+int tsm2x_set_kernel_events(void* start_event, void* stop_event) {
+  t_ev_start = reinterpret_cast<cudaEvent_t>(start_event);
+  t_ev_stop = reinterpret_cast<cudaEvent_t>(stop_event);
+  return TSM2X_OK;
 }
 
 const char* tsm2x_last_error(void) { return t_err.c_str(); }

@@ -1,0 +1,84 @@
+"""Multi-GPU driver: row-sharded TSM2R / TSM2L, one process per GPU.
+
+A (m x k) and C (m x n) are split into contiguous row shards, rank r owning rows
+[r0, r1) = row_partition(m, world, r). B (k x n, small) lives on the source rank and is
+broadcast once per call over NCCL (NVLink / NVSwitch); every rank then runs the single-GPU
+kernel on its shard. Rows of C are independent (reference SPEC.md:262), so there is no
+reduction and no other exchange; an optional gather assembles C on one rank.
+
+The communication is plain ``torch.distributed`` (backend "nccl" on GPUs). The local compute
+is :func:`paper_2002_03258_b200.gemm`; tests inject a CPU stand-in to exercise the sharding /
+broadcast / gather logic with the gloo backend on CPU.
+"""
+
+from __future__ import annotations
+
+from typing import Callable, Optional, Tuple
+
+ROW_ALIGN = 32  # shard boundaries on 32-row multiples keep every shard's columns 256-B aligned
+
+
+def row_partition(m: int, world: int, rank: int, align: int = ROW_ALIGN) -> Tuple[int, int]:
+    """Contiguous row range of ``rank``: balanced in units of ``align`` rows (the last shard
+    takes the ragged tail). Every row is owned by exactly one rank."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError(f"bad rank {rank} for world size {world}")
+    blocks = (m + align - 1) // align
+    b0 = blocks * rank // world
+    b1 = blocks * (rank + 1) // world
+    return min(m, b0 * align), min(m, b1 * align)
+
+
+def colmajor_buffer(rows: int, cols: int, dtype, device):
+    """A dense (rows x cols) column-major tensor (ld == rows) whose storage is one contiguous
+    block, so it can be passed to collectives directly."""
+    import torch
+    return torch.empty((cols, rows), dtype=dtype, device=device).t()
+
+
+def broadcast_b(B, k: int, n: int, dtype, device, src: int = 0, group=None):
+    """Returns the k x n column-major B on every rank (rank ``src`` passes its B, others None)."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group) if group is not None else dist.get_rank()
+    buf = colmajor_buffer(k, n, dtype, device)
+    if rank == src:
+        buf.copy_(B)
+    dist.broadcast(buf.t(), src=src, group=group)  # .t() is the contiguous (n, k) storage
+    return buf
+
+
+def run_sharded(A_local, B, C_local, *, k: int, n: int, variant="v3", c_is_zero: bool = False, src: int = 0,
+                group=None, compute: Optional[Callable] = None):
+    """One distributed call: broadcast B from ``src``, then C_local (+)= A_local @ B on each rank.
+
+    ``A_local``/``C_local`` are this rank's row shards (column-major). Returns (C_local, B_local).
+    """
+    Bl = broadcast_b(B, k, n, A_local.dtype, A_local.device, src=src, group=group)
+    if compute is None:
+        from .kernels import gemm
+        gemm(A_local, Bl, C_local, variant=variant, c_is_zero=c_is_zero)
+    else:
+        compute(A_local, Bl, C_local, c_is_zero)
+    return C_local, Bl
+
+
+def gather_c(C_local, m: int, n: int, dst: int = 0, group=None):
+    """Assembles the full m x n C (column-major) on ``dst``; other ranks get None."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if group is not None else dist.get_world_size()
+    rank = dist.get_rank(group) if group is not None else dist.get_rank()
+    shard_rows = [row_partition(m, world, r) for r in range(world)]
+    maxr = max(r1 - r0 for r0, r1 in shard_rows)
+    pad = torch.zeros((n, maxr), dtype=C_local.dtype, device=C_local.device)
+    r0, r1 = shard_rows[rank]
+    pad[:, : r1 - r0] = C_local.t()
+    gathered = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
+    dist.gather(pad, gather_list=gathered, dst=dst, group=group)
+    if rank != dst:
+        return None
+    full = colmajor_buffer(m, n, C_local.dtype, C_local.device)
+    for r, (a, b) in enumerate(shard_rows):
+        full[a:b] = gathered[r][:, : b - a].t()
+    return full

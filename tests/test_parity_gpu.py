@@ -149,7 +149,7 @@ def test_l_opt2_device_check():
     import torch
     tsm = _tsm()
     A = torch.ones((64, 4), dtype=torch.float64, device="cuda").t().contiguous().t()
-    B = torch.ones((4, 4), dtype=torch.float64, device="cuda")
+    B = torch.ones((4, 4), dtype=torch.float64, device="cuda").t()
     C = torch.ones((64, 4), dtype=torch.float64, device="cuda").t().contiguous().t()
     with pytest.raises(ValueError):
         tsm.gemm(A, B, C, variant="l-opt2", check_zero_c=True)
