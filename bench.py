@@ -1,0 +1,407 @@
+#!/usr/bin/env python
+"""Benchmark — BASELINE.json metric "TSM2R/TSM2L fp64 GFLOP/s and achieved HBM GB/s (% roofline)".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload ...]
+  torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Workload (N=1): BASELINE configs[1] at its headline point — TSM2R fp64, reference naming
+A m x k = 30720 x 30720, B k x n = 30720 x 8 (BASELINE naming n=30720, k=8), C m x n,
+C += A*B. One "step" = one full TSM2R call over that problem with A resident in HBM
+(7.55 GB, 60x the 126 MB L2, so no L2 flush is needed between steps).
+N > 1: weak scaling — every rank owns a 30720-row shard of a (30720*N) x 30720 A (generated on
+its device with the shared counter-based generator), B is broadcast from rank 0 over NCCL every
+step (the path's one exchange), then each rank runs the kernel on its shard. Time = max over
+ranks of the device-event time of the K steps.
+
+The JSON line also carries: roofline (dominant kernel, CUDA events around each launch),
+cpu_baseline (the reference CPU path restated in numpy — oracle/ — on a bounded row sample, rank 0,
+N=1), e2e (same metric through the host-buffer C ABI tsm2x_run_host with pinned host buffers,
+H2D of A and D2H of C inside the timed region), clocks (NVML samples during the timed region),
+gpu_launches (libtsm2x launches in the timed region).
+
+--impl reference: the reference's CPU implementation of the path (run_native's vectorised body,
+kernels.py:391-416, restated in oracle/reference.py — the reference is pure Python and has no
+compiled form) on all host threads, rank 0 only, bounded row sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TSM2R/TSM2L fp64 GFLOP/s and achieved HBM GB/s (% roofline) at 1/2/4/8 B200"
+UNIT = "GFLOP/s"
+
+WORKLOADS = {
+    # name: (rows per GPU m, k, n, precision, variant, c_is_zero, description)
+    "tsm2r_fp64_n8": (30720, 30720, 8, "double", "v3", False,
+                      "TSM2R fp64, ref (m,k,n)=(30720,30720,8) = BASELINE configs[1] n=30720,k=8; C += A*B"),
+    "tsm2r_fp64_n2": (30720, 30720, 2, "double", "v3", False, "TSM2R fp64 BASELINE configs[1] k=2"),
+    "tsm2r_fp64_n4": (30720, 30720, 4, "double", "v3", False, "TSM2R fp64 BASELINE configs[1] k=4"),
+    "tsm2r_fp64_n16": (30720, 30720, 16, "double", "v3", False, "TSM2R fp64 BASELINE configs[1] k=16"),
+    "tsm2l_fp64": (1 << 24, 16, 16, "double", "l-opt2", True,
+                   "TSM2L fp64 A 2^24x16, B 16x16, C = A*B (L_OPT2 zero-C contract), BASELINE configs[2]"),
+    "tsm2r_fp32_n16": (32768, 32768, 16, "single", "v3", False, "TSM2R fp32 BASELINE configs[3]"),
+    "tsm2r_fp64_n8_65536": (65536, 65536, 8, "double", "v3", False, "TSM2R fp64 BASELINE configs[4] per GPU"),
+}
+
+
+def algorithmic(m, k, n, eb, c_is_zero):
+    """flops = 2mkn; bytes = eb*(mk + kn + 2mn) (C read+write) or eb*(mk+kn+mn)."""
+    flops = 2.0 * m * k * n
+    byts = eb * (m * k + k * n + (1 if c_is_zero else 2) * m * n)
+    return flops, byts
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload):
+    """dram bytes read+write per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        e = d.get(workload)
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and clock-event reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clocks"}
+
+    def __init__(self, device_index, period=0.01):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for b, name in self.REASONS.items():
+                    if bits & b:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "nvml")}
+        busy = [s for s in self.samples] or [0]
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------------
+def cpu_sample_inputs(m, k, n, prec, c_is_zero, rows, cols):
+    """A (rows x cols) corner of the workload's A (+ matching B rows, C rows), regenerated on the
+    host by the shared generator. The reference's per-element work (and so its GFLOP/s) is the
+    same for any such sample; sampling columns keeps each numpy call as large as in the full run."""
+    import numpy as np
+
+    from oracle.rng import uniform_block
+    dt = np.float64 if prec == "double" else np.float32
+    rows, cols = min(rows, m), min(cols, k)
+    A = uniform_block(range(rows), range(cols), 1, dt)
+    B = uniform_block(range(cols), range(n), 2, dt)
+    C = np.zeros((rows, n), dt) if c_is_zero else uniform_block(range(rows), range(n), 3, dt)
+    return A, B, C
+
+
+def cpu_time(A, B, C, threads, cols=None):
+    """Seconds for the reference CPU path (oracle restatement of run_native) on the first cols."""
+    from oracle import run_native_port_threaded
+    cols = A.shape[1] if cols is None else cols
+    t0 = time.perf_counter()
+    run_native_port_threaded(A[:, :cols], B[:cols], C, threads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_sample_shape(m, k, max_elems=1 << 25):
+    """Rows x cols of the CPU sample: whole rows up to 30720 (TSM2R) and as many columns as fit
+    max_elems; for TSM2L (tiny k) all columns and a row slab."""
+    if k > 64:
+        rows = min(m, 30720)
+        cols = min(k, max(1, max_elems // rows))
+    else:
+        cols = k
+        rows = min(m, max(1, max_elems // k))
+    return rows, cols
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference_arm(args, wl):
+    m, k, n, prec, variant, c_is_zero, desc = WORKLOADS[wl]
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = host_threads()
+    rows, cols = cpu_sample_shape(m, k)
+    A, B, C = cpu_sample_inputs(m, k, n, prec, c_is_zero, rows, cols)
+    # calibrate the columns per step so warmup + steps finish in about two minutes
+    c0 = min(cols, 64)
+    t0 = min(cpu_time(A, B, C, threads, c0) for _ in range(2))
+    per_step_budget = max(0.05, 120.0 / max(1, args.steps + args.warmup))
+    cs = int(max(min(cols, 8), min(cols, c0 * per_step_budget / max(t0, 1e-6))))
+    for _ in range(args.warmup):
+        cpu_time(A, B, C, threads, cs)
+    times = [cpu_time(A, B, C, threads, cs) for _ in range(args.steps)]
+    tot = sum(times)
+    value = 2.0 * rows * cs * n * len(times) / tot / 1e9
+    sample = (f"A[:{rows}, :{cs}] of the {m} x {k} A per step (n={n}, {prec}); reference run_native body "
+              f"(kernels.py:391-416) restated in numpy (oracle/reference.py), row slabs on {threads} threads")
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / len(times), 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if prec == "double" else "f32", "data": "synthetic (counter-based U[0,1))",
+            "config": {"workload": desc, "m": m, "k": k, "n": n},
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+def run_ours(args, wl):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2002_03258_b200 as tsm
+    from paper_2002_03258_b200 import _lib
+    from paper_2002_03258_b200.multi import broadcast_b
+
+    m, k, n, prec, variant, c_is_zero, desc = WORKLOADS[wl]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    dt = torch.float64 if prec == "double" else torch.float32
+    eb = 8 if prec == "double" else 4
+    lib = _lib.load()
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- inputs resident in HBM (rank shard of a (m*world) x k matrix)
+    r0 = rank * m
+    A = tsm.colmajor_empty(m, k, dt, dev)
+    tsm.fill_uniform(A, seed=1, row_offset=r0)
+    B = tsm.colmajor_empty(k, n, dt, dev)
+    tsm.fill_uniform(B, seed=2)
+    C = tsm.colmajor_empty(m, n, dt, dev)
+    if c_is_zero:
+        C.zero_()
+    else:
+        tsm.fill_uniform(C, seed=3, row_offset=r0)
+    torch.cuda.synchronize()
+
+    def step(Bsrc, kev=None):
+        Bl = broadcast_b(Bsrc if rank == 0 else None, k, n, dt, dev) if world > 1 else Bsrc
+        if kev is not None:
+            lib.tsm2x_set_kernel_events(ctypes.c_void_p(kev[0].cuda_event), ctypes.c_void_p(kev[1].cuda_event))
+        tsm.gemm(A, Bl, C, variant=variant, c_is_zero=c_is_zero)
+
+    for _ in range(args.warmup):
+        step(B)
+    kevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a_, b_ in kevs:  # materialise the CUDA events before handing them to the library
+        a_.record(stream)
+        b_.record(stream)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for i in range(args.steps):
+            step(B, kevs[i])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    ms_total = t0.elapsed_time(t1)
+    kern_ms = sum(a_.elapsed_time(b_) for a_, b_ in kevs) / args.steps
+    if world > 1:
+        t = torch.tensor([ms_total, kern_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total, kern_ms = float(t[0]), float(t[1])
+    flops, byts = algorithmic(m, k, n, eb, c_is_zero)
+    ms_step = ms_total / args.steps
+    value = flops * world / (ms_step * 1e-3) / 1e9
+    gbps = byts * world / (ms_step * 1e-3) / 1e9
+    peak, peak_src = measured_peaks()
+    kern_gbps = byts / (kern_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(wl)
+
+    # ---- e2e through the host-buffer C ABI (pinned host buffers)
+    e2e = None
+    if args.e2e_steps > 0:
+        e2e = run_e2e(args, A, B, C, m, k, n, dt, eb, variant, c_is_zero, world, rank, dev)
+
+    # ---- CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = host_threads()
+        rows, cols = cpu_sample_shape(m, k, args.cpu_elems)
+        Ah, Bh, Chh = cpu_sample_inputs(m, k, n, prec, c_is_zero, rows, cols)
+        t = min(cpu_time(Ah, Bh, Chh, threads) for _ in range(2))
+        rate = 2.0 * rows * cols * n / t / 1e9
+        del Ah, Bh, Chh
+        cpu = {"value": round(rate, 4), "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"A[:{rows}, :{cols}] of the {m} x {k} A (n={n}, {prec}), best of 2; reference run_native body "
+                         f"(kernels.py:391-416) restated in numpy (oracle/reference.py) on {threads} threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64" if prec == "double" else "f32",
+            "data": "synthetic: counter-based U[0,1) generated on device (oracle/rng.py regenerates any slab)",
+            "config": {"workload": desc, "m_per_gpu": m, "m_total": m * world, "k": k, "n": n,
+                       "naming": "reference (m,k,n), skinny n (SURVEY.md G1)",
+                       "parallelism": f"row-shard x{world}" + (", B broadcast per step (NCCL)" if world > 1 else ""),
+                       "l2": f"inputs larger than L2 (A {m * k * eb / 1e9:.2f} GB per GPU vs 0.126 GB L2), no flush",
+                       "bytes_form": "eb*(mk+kn+mn) C write-only" if c_is_zero else "eb*(mk+kn+2mn) C read+write"},
+            "GBps": round(gbps, 1),
+            "roofline": {"bound": "hbm", "achieved": round(kern_gbps, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(kern_gbps / peak, 4), "traffic": traffic,
+                         "kernel": "tsm2r_stream_tma" if k > 64 else "tsm2l_kernel",
+                         "kernel_ms": round(kern_ms, 5), "algorithmic_bytes_per_launch": byts,
+                         "peak_source": peak_src,
+                         "read_stream_ceiling_gbs": 7300.0,
+                         "frac_of_read_stream": round(kern_gbps / 7300.0, 4)},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, A, B, C, m, k, n, dt, eb, variant, c_is_zero, world, rank, dev):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2002_03258_b200 import _lib
+    from paper_2002_03258_b200.core import Variant
+    lib = _lib.load()
+    try:
+        hA = torch.empty((k, m), dtype=dt, pin_memory=True)  # (k, m) row-major == A column-major, lda=m
+        pinned = True
+    except Exception:
+        hA = torch.empty((k, m), dtype=dt)
+        pinned = False
+    hA.copy_(A.t())
+    hB = B.t().contiguous().cpu().pin_memory()      # (n, k) row-major == B column-major, ldb=k
+    hC = torch.empty((n, m), dtype=dt, pin_memory=True)
+    hC.copy_(C.t())
+    hOut = torch.empty((n, m), dtype=dt, pin_memory=True)
+    p = _lib.Params(128, 1, 4, 1, Variant.parse(variant).ordinal)
+    flags = _lib.FLAG_C_IS_ZERO if c_is_zero else 0
+    precision = _lib.DOUBLE if dt == torch.float64 else _lib.SINGLE
+
+    def call():
+        rc = lib.tsm2x_run_host(Variant.parse(variant).ordinal, precision, m, k, n, hA.data_ptr(), m,
+                                hB.data_ptr(), k, hC.data_ptr(), hOut.data_ptr(), m, ctypes.byref(p), flags,
+                                torch.cuda.current_device())
+        _lib.check(rc)
+
+    call()  # warm-up (allocations, staging)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        call()
+    t = (time.perf_counter() - t0) / args.e2e_steps
+    if world > 1:
+        tt = torch.tensor([t], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt[0])
+    flops, _ = algorithmic(m, k, n, eb, c_is_zero)
+    h2d = eb * (k * m + k * n + (0 if c_is_zero else m * n))
+    d2h = eb * m * n
+    return {"value": round(flops * world / t / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": round(t * 1e3, 3), "steps": args.e2e_steps,
+            "host_buffers": "pinned" if pinned else "pageable",
+            "api": "tsm2x_run_host (C ABI drop-in for run_native), H2D of A pipelined with the kernels"}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="tsm2r_fp64_n8")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-elems", type=int, default=1 << 26, help="elements of A in the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference_arm(args, args.workload)
+    else:
+        run_ours(args, args.workload)
+
+
+if __name__ == "__main__":
+    main()

@@ -244,25 +244,82 @@ static int run_ablation(int variant, int64_t m, int64_t k, int64_t n, const T* A
 }
 
 // ---- TSM2R pass: C[:, p:p+w] (+)= A * B[:, p:p+w] -----------------------------------------
+// Bt (this pass of B, row-major, zero padded to kpad rows) at the front of the workspace.
 template <typename T, int NT>
-static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m, int64_t k, int w, const T* A,
-                          int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc, bool c_is_zero, cudaStream_t s) {
-  constexpr int THREADS = 256;
+static int stage_bt(Workspace* ws, int64_t k, int64_t kpad, int w, const T* B, int64_t ldb, size_t extra_bytes,
+                    size_t counters, cudaStream_t s, T** Bt, char** rest) {
+  const size_t bt_bytes = align_up((size_t)kpad * NT * sizeof(T), 256);
+  TSM2X_TRY(ws_reserve(ws, bt_bytes + extra_bytes, counters, s));
+  *Bt = reinterpret_cast<T*>(ws->buf);
+  *rest = static_cast<char*>(ws->buf) + bt_bytes;
+  const int64_t tot = kpad * NT;
+  prep_bt<T, NT><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(B, ldb, k, kpad, w, *Bt);
+  return check_launch("prep_bt");
+}
+
+// TMA flavour: dynamic items, deterministic combine (tsm2r_tma.cuh)
+template <typename T, int NT>
+static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k, int w, const T* A, int64_t lda,
+                         const T* B, int64_t ldb, T* C, int64_t ldc, bool c_is_zero, cudaStream_t s) {
+  using Cfg = TmaCfg<T, NT>;
+  auto kern = tsm2r_stream_tma<T, NT>;
+  TSM2X_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  const int occ = occupancy(kern, Cfg::THREADS, Cfg::SMEM);
+  const int64_t G_full = (int64_t)di.sms * occ;
+  DynArgs<T> a;
+  a.C = C;
+  a.ldc = ldc;
+  a.m = m;
+  a.k = k;
+  a.w = w;
+  a.c_is_zero = c_is_zero ? 1 : 0;
+  a.num_rb = (m + Cfg::R - 1) / Cfg::R;
+  // ~24 items per CTA so the dynamic queue can even out per-SM bandwidth differences; chunks of
+  // at least 256 columns keep the partial-slot traffic (2*NT/kch of A's bytes, L2 only) small
+  const int64_t want_items = 24 * G_full;
+  int64_t nch = std::max<int64_t>(1, (want_items + a.num_rb - 1) / a.num_rb);
+  int64_t kch = (int64_t)align_up((size_t)((k + nch - 1) / nch), Cfg::KC);
+  kch = std::max<int64_t>(kch, std::min<int64_t>(256, (int64_t)align_up((size_t)k, Cfg::KC)));
+  a.kch = kch;
+  a.nch = (k + kch - 1) / kch;
+  a.items = a.num_rb * a.nch;
+  a.defer = a.nch > 128 ? 1 : 0;
+  const int64_t G = std::min<int64_t>(G_full, a.items);
+  const int64_t kpad = (int64_t)align_up((size_t)k, Cfg::KC);
+  const size_t slots = a.nch > 1 ? (size_t)a.items * NT * Cfg::R * sizeof(T) : 0;
+  T* Bt;
+  char* rest;
+  TSM2X_TRY((stage_bt<T, NT>(ws, k, kpad, w, B, ldb, slots, (size_t)a.num_rb + 4, s, &Bt, &rest)));
+  a.Bt = Bt;
+  a.ws = reinterpret_cast<T*>(rest);
+  a.queue = ws->counters;          // [0..1] 64-bit item counter, [2] producers finished
+  a.counters = ws->counters + 4;   // per row block arrivals
+  alignas(64) CUtensorMap tmap;
+  TSM2X_TRY(encode_a_map(&tmap, A, m, k, lda, sizeof(T), Cfg::BOX, Cfg::KC));
+  const bool timed = t_ev_start && t_ev_stop;
+  if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
+  void* args[] = {&a, &tmap};
+  TSM2X_CUDA(cudaLaunchKernel((const void*)kern, dim3((unsigned)G), dim3(Cfg::THREADS), args, Cfg::SMEM, s));
+  TSM2X_TRY(check_launch("tsm2r_stream_tma"));
+  if (timed) {
+    TSM2X_CUDA(cudaEventRecord(t_ev_stop, s));
+    t_ev_start = t_ev_stop = nullptr;
+  }
+  if (a.defer) {
+    dim3 grid((unsigned)((Cfg::R + 255) / 256), (unsigned)a.num_rb);
+    reduce_items<T, NT, Cfg::R><<<grid, 256, 0, s>>>(a);
+    TSM2X_TRY(check_launch("reduce_items"));
+  }
+  return TSM2X_OK;
+}
+
+// LDG flavour: static stream-K (any alignment; the fallback when TMA's 16-byte rules fail)
+template <typename T, int NT>
+static int run_tsm2r_ldg(const DevInfo& di, Workspace* ws, int64_t m, int64_t k, int w, const T* A, int64_t lda,
+                         const T* B, int64_t ldb, T* C, int64_t ldc, bool c_is_zero, cudaStream_t s) {
+  constexpr int THREADS = 256, P = 8, KC = 32;
   const bool vec = aligned16(A) && (lda % Vec<T>::N == 0);
-  const int rpt = vec ? Vec<T>::N : 1;
-  // TMA flavour needs 16B-aligned column starts (lda*eb % 16 == 0) and the vector layout
-  const bool tma_ok = vec && ((lda * (int64_t)sizeof(T)) % 16 == 0) && m < (int64_t(1) << 31) &&
-                      k < (int64_t(1) << 31);
-  if (impl == TSM2X_IMPL_AUTO) impl = tma_ok ? TSM2X_IMPL_STREAM_TMA : TSM2X_IMPL_STREAM_LDG;
-  if (impl == TSM2X_IMPL_STREAM_TMA && !tma_ok) impl = TSM2X_IMPL_STREAM_LDG;
-  const bool tma = impl == TSM2X_IMPL_STREAM_TMA;
-
-  const int R = tma ? TmaCfg<T, NT>::R : THREADS * rpt;
-  const int KC = tma ? TmaCfg<T, NT>::KC : 32;
-  const int64_t num_rb = (m + R - 1) / R;
-  const int64_t num_kb = (k + KC - 1) / KC;
-  const int64_t units = num_rb * num_kb;
-
+  const int R = THREADS * (vec ? Vec<T>::N : 1);
   StreamArgs<T> a;
   a.A = A;
   a.lda = lda;
@@ -272,29 +329,18 @@ static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m,
   a.k = k;
   a.w = w;
   a.c_is_zero = c_is_zero ? 1 : 0;
-  a.num_rb = num_rb;
+  a.num_rb = (m + R - 1) / R;
   a.KC = KC;
-
-  int occ;
+  const int64_t num_kb = (k + KC - 1) / KC;
+  const int64_t units = a.num_rb * num_kb;
   const void* kfn;
-  size_t smem = 0;
-  int threads;
-  if (tma) {
-    auto kern = tsm2r_stream_tma<T, NT>;
-    smem = TmaCfg<T, NT>::SMEM;
-    threads = TmaCfg<T, NT>::THREADS;
-    cudaError_t attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    TSM2X_CUDA(attr_err);
-    occ = occupancy(kern, threads, smem);
-    kfn = (const void*)kern;
-  } else if (vec) {
-    auto kern = tsm2r_stream_ldg<T, NT, THREADS, 8, true>;
-    threads = THREADS;
+  int occ;
+  if (vec) {
+    auto kern = tsm2r_stream_ldg<T, NT, THREADS, P, true>;
     occ = occupancy(kern, THREADS, 0);
     kfn = (const void*)kern;
   } else {
-    auto kern = tsm2r_stream_ldg<T, NT, THREADS, 8, false>;
-    threads = THREADS;
+    auto kern = tsm2r_stream_ldg<T, NT, THREADS, P, false>;
     occ = occupancy(kern, THREADS, 0);
     kfn = (const void*)kern;
   }
@@ -302,52 +348,46 @@ static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m,
   a.part.units = units;
   a.part.num_kb = num_kb;
   a.part.G = G;
-  // many-way splits (few long row blocks) are combined by a separate parallel kernel
   const int64_t max_contrib = (num_kb * G + units - 1) / units + 1;
   a.defer = (max_contrib > 24) ? 1 : 0;
-
-  const int64_t kpad = num_kb * KC;
-  const size_t bt_bytes = align_up((size_t)kpad * NT * sizeof(T), 256);
   const size_t part_bytes = (size_t)G * 2 * NT * R * sizeof(T);
-  TSM2X_TRY(ws_reserve(ws, bt_bytes + part_bytes, (size_t)num_rb, s));
-  T* Bt = reinterpret_cast<T*>(ws->buf);
+  T* Bt;
+  char* rest;
+  TSM2X_TRY((stage_bt<T, NT>(ws, k, num_kb * KC, w, B, ldb, part_bytes, (size_t)a.num_rb + 4, s, &Bt, &rest)));
   a.Bt = Bt;
-  a.ws = reinterpret_cast<T*>(static_cast<char*>(ws->buf) + bt_bytes);
-  a.counters = ws->counters;
-
-  {
-    const int64_t tot = kpad * NT;
-    const int bs = 256;
-    prep_bt<T, NT><<<(unsigned)((tot + bs - 1) / bs), bs, 0, s>>>(B, ldb, k, kpad, w, Bt);
-    TSM2X_TRY(check_launch("prep_bt"));
-  }
-  alignas(64) CUtensorMap tmap;
+  a.ws = reinterpret_cast<T*>(rest);
+  a.counters = ws->counters + 4;
   const bool timed = t_ev_start && t_ev_stop;
   if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
-  if (tma) {
-    TSM2X_TRY(encode_a_map(&tmap, A, m, k, lda, sizeof(T), TmaCfg<T, NT>::BOX, KC));
-    void* args[] = {&a, &tmap};
-    TSM2X_CUDA(cudaLaunchKernel(kfn, dim3((unsigned)G), dim3(threads), args, smem, s));
-  } else {
-    void* args[] = {&a};
-    TSM2X_CUDA(cudaLaunchKernel(kfn, dim3((unsigned)G), dim3(threads), args, smem, s));
-  }
-  TSM2X_TRY(check_launch("tsm2r_stream"));
+  void* args[] = {&a};
+  TSM2X_CUDA(cudaLaunchKernel(kfn, dim3((unsigned)G), dim3(THREADS), args, 0, s));
+  TSM2X_TRY(check_launch("tsm2r_stream_ldg"));
   if (timed) {
     TSM2X_CUDA(cudaEventRecord(t_ev_stop, s));
     t_ev_start = t_ev_stop = nullptr;
   }
   if (a.defer) {
-    dim3 grid((unsigned)((R + 255) / 256), (unsigned)num_rb);
-    switch (R) {
-      case 256: reduce_partials<T, NT, 256><<<grid, 256, 0, s>>>(a); break;
-      case 512: reduce_partials<T, NT, 512><<<grid, 256, 0, s>>>(a); break;
-      case 1024: reduce_partials<T, NT, 1024><<<grid, 256, 0, s>>>(a); break;
-      default: return fail(TSM2X_EUNSUPPORTED, "no reduce kernel for R=%d", R);
-    }
+    dim3 grid((unsigned)((R + 255) / 256), (unsigned)a.num_rb);
+    if (R == 256)
+      reduce_partials<T, NT, 256><<<grid, 256, 0, s>>>(a);
+    else if (R == 512)
+      reduce_partials<T, NT, 512><<<grid, 256, 0, s>>>(a);
+    else
+      reduce_partials<T, NT, 1024><<<grid, 256, 0, s>>>(a);
     TSM2X_TRY(check_launch("reduce_partials"));
   }
   return TSM2X_OK;
+}
+
+template <typename T, int NT>
+static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m, int64_t k, int w, const T* A,
+                          int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc, bool c_is_zero, cudaStream_t s) {
+  // TMA needs 16-byte aligned base and column stride; coordinates are int32
+  const bool tma_ok = aligned16(A) && ((lda * (int64_t)sizeof(T)) % 16 == 0) && m < (int64_t(1) << 31) &&
+                      k < (int64_t(1) << 31);
+  const bool tma = (impl == TSM2X_IMPL_AUTO || impl == TSM2X_IMPL_STREAM_TMA) && tma_ok;
+  if (tma) return run_tsm2r_tma<T, NT>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, s);
+  return run_tsm2r_ldg<T, NT>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, s);
 }
 
 // ---- TSM2L pass ------------------------------------------------------------------------------
@@ -518,71 +558,96 @@ static void par_copy2d(void* dst, size_t dpitch, const void* src, size_t spitch,
   for (auto& x : th) x.join();
 }
 
-struct HostRun {
-  int dev = 0;
+// Per-device resources of the host path, kept across calls (allocation and stream creation
+// would otherwise cost more than the copies): three streams, named device / pinned buffers that
+// only grow, and an event pool. One call at a time per device (mutex).
+struct HostCtx {
+  std::mutex mu;
+  int dev = -1;
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
-  std::vector<void*> dev_allocs;
-  std::vector<void*> host_allocs;
+  std::map<std::string, std::pair<void*, size_t>> dbufs, hbufs;
   std::vector<cudaEvent_t> events;
-  ~HostRun() {
-    if (comp) cudaStreamSynchronize(comp);
-    if (h2d) cudaStreamSynchronize(h2d);
-    if (d2h) cudaStreamSynchronize(d2h);
-    for (auto p : dev_allocs) cudaFree(p);
-    for (auto p : host_allocs) cudaFreeHost(p);
-    for (auto e : events) cudaEventDestroy(e);
-    if (h2d) cudaStreamDestroy(h2d);
-    if (comp) cudaStreamDestroy(comp);
-    if (d2h) cudaStreamDestroy(d2h);
-  }
-  int init() {
+  size_t ev_next = 0;
+  int init(int device) {
+    if (h2d) return TSM2X_OK;
+    dev = device;
     TSM2X_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
     TSM2X_CUDA(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking));
     TSM2X_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
     return TSM2X_OK;
   }
-  int dmalloc(void** p, size_t bytes) {
-    if (cudaMalloc(p, bytes) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(TSM2X_ENOMEM, "device allocation of %zu bytes failed", bytes);
+  int dbuf(const std::string& name, size_t bytes, void** p) {
+    auto& e = dbufs[name];
+    if (e.second < bytes) {
+      if (e.first) TSM2X_CUDA(cudaFree(e.first));
+      e = {nullptr, 0};
+      if (cudaMalloc(&e.first, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        e.first = nullptr;
+        return fail(TSM2X_ENOMEM, "device allocation of %zu bytes failed", bytes);
+      }
+      e.second = bytes;
     }
-    dev_allocs.push_back(*p);
+    *p = e.first;
     return TSM2X_OK;
   }
-  int hmalloc(void** p, size_t bytes) {
-    if (cudaMallocHost(p, bytes) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(TSM2X_ENOMEM, "pinned allocation of %zu bytes failed", bytes);
+  int hbuf(const std::string& name, size_t bytes, void** p) {
+    auto& e = hbufs[name];
+    if (e.second < bytes) {
+      if (e.first) TSM2X_CUDA(cudaFreeHost(e.first));
+      e = {nullptr, 0};
+      if (cudaMallocHost(&e.first, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        e.first = nullptr;
+        return fail(TSM2X_ENOMEM, "pinned allocation of %zu bytes failed", bytes);
+      }
+      e.second = bytes;
     }
-    host_allocs.push_back(*p);
+    *p = e.first;
     return TSM2X_OK;
   }
   int event(cudaEvent_t* e) {
-    TSM2X_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    events.push_back(*e);
+    if (ev_next == events.size()) {
+      cudaEvent_t x;
+      TSM2X_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+      events.push_back(x);
+    }
+    *e = events[ev_next++];
     return TSM2X_OK;
   }
+  void begin() { ev_next = 0; }
+  void drain() {
+    cudaStreamSynchronize(h2d);
+    cudaStreamSynchronize(comp);
+    cudaStreamSynchronize(d2h);
+  }
 };
+static std::mutex g_host_mu;
+static std::map<int, std::unique_ptr<HostCtx>> g_host;
+
+static HostCtx* host_ctx(int dev) {
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  auto& slot = g_host[dev];
+  if (!slot) slot.reset(new HostCtx());
+  return slot.get();
+}
 
 // copy a 2-D host block (width bytes x height rows, host pitch) to the device, via pinned
-// staging when the source is pageable. Ordered on `st`.
+// staging (filled by host threads) when the source is pageable. Ordered on `st`.
 struct Stager {
-  HostRun* hr;
-  bool pinned_src;
-  std::vector<void*> stage;
-  std::vector<cudaEvent_t> done;
-  size_t stage_bytes = 0;
+  HostCtx* hc = nullptr;
+  bool pinned_src = true;
+  void* stage[2] = {nullptr, nullptr};
+  cudaEvent_t done[2];
+  bool used[2] = {false, false};
   int next = 0;
-  int init(HostRun* h, bool pinned, size_t max_block, int nstage) {
-    hr = h;
+  int init(HostCtx* h, bool pinned, size_t max_block, const char* tag) {
+    hc = h;
     pinned_src = pinned;
     if (pinned) return TSM2X_OK;
-    stage_bytes = max_block;
-    stage.resize(nstage);
-    done.resize(nstage);
-    for (int i = 0; i < nstage; ++i) {
-      TSM2X_TRY(hr->hmalloc(&stage[i], stage_bytes));
-      TSM2X_TRY(hr->event(&done[i]));
+    for (int i = 0; i < 2; ++i) {
+      TSM2X_TRY(hc->hbuf(std::string(tag) + char('0' + i), max_block, &stage[i]));
+      TSM2X_TRY(hc->event(&done[i]));
     }
     return TSM2X_OK;
   }
@@ -591,12 +656,13 @@ struct Stager {
       TSM2X_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyHostToDevice, st));
       return TSM2X_OK;
     }
-    int i = next;
-    next = (next + 1) % (int)stage.size();
-    TSM2X_CUDA(cudaEventSynchronize(done[i]));  // staging buffer i free again
+    const int i = next;
+    next ^= 1;
+    if (used[i]) TSM2X_CUDA(cudaEventSynchronize(done[i]));  // staging buffer i free again
     par_copy2d(stage[i], width, src, spitch, width, height);
     TSM2X_CUDA(cudaMemcpy2DAsync(dst, dpitch, stage[i], width, width, height, cudaMemcpyHostToDevice, st));
     TSM2X_CUDA(cudaEventRecord(done[i], st));
+    used[i] = true;
     return TSM2X_OK;
   }
 };
@@ -616,94 +682,100 @@ static int run_host_t(int variant, int64_t m, int64_t k, int64_t n, const T* A, 
         if (Cin[i + j * ldc] != T(0)) return fail(TSM2X_EINVAL, "L_OPT2 stores partial sums to C and requires a zeroed C");
     c_is_zero = true;
   }
-  HostRun hr;
-  hr.dev = device;
-  TSM2X_TRY(hr.init());
+  HostCtx* hc = host_ctx(device);
+  std::lock_guard<std::mutex> lk(hc->mu);
+  TSM2X_TRY(hc->init(device));
+  hc->begin();
+  struct Drain {
+    HostCtx* h;
+    ~Drain() { h->drain(); }
+  } drain_on_exit{hc};
   const size_t eb = sizeof(T);
   const int64_t ldd = (int64_t)align_up((size_t)m, 32);  // padded device leading dimension
   const bool pinnedA = is_pinned(A);
   const bool use_l = k <= TSM2L_KMAX;
+  const int dev_variant = (variant == TSM2X_L_OPT2) ? TSM2X_L_OPT1 : variant;  // zero-C handled by flags
 
-  // B on the device (tiny)
   T* dB;
-  TSM2X_TRY(hr.dmalloc((void**)&dB, (size_t)k * n * eb));
-  TSM2X_CUDA(cudaMemcpy2DAsync(dB, k * eb, B, ldb * eb, k * eb, n, cudaMemcpyHostToDevice, hr.h2d));
+  TSM2X_TRY(hc->dbuf("B", (size_t)k * n * eb, (void**)&dB));
+  TSM2X_CUDA(cudaMemcpy2DAsync(dB, k * eb, B, ldb * eb, k * eb, n, cudaMemcpyHostToDevice, hc->h2d));
+  cudaEvent_t b_ready;
+  TSM2X_TRY(hc->event(&b_ready));
+  TSM2X_CUDA(cudaEventRecord(b_ready, hc->h2d));
+  TSM2X_CUDA(cudaStreamWaitEvent(hc->comp, b_ready, 0));
 
   const size_t slab_target = (size_t)256 << 20;
   if (!use_l) {
-    // ---- TSM2R: column slabs of A, C resident on the device
+    // ---- TSM2R: column slabs of A stream in while earlier slabs are multiplied; C stays on
+    // the device (C += A[:, slab] * B[slab, :] per slab)
     T* dC;
-    TSM2X_TRY(hr.dmalloc((void**)&dC, (size_t)ldd * n * eb));
-    if (!c_is_zero)
-      TSM2X_CUDA(cudaMemcpy2DAsync(dC, ldd * eb, Cin, ldc * eb, m * eb, n, cudaMemcpyHostToDevice, hr.h2d));
+    TSM2X_TRY(hc->dbuf("C", (size_t)ldd * n * eb, (void**)&dC));
+    if (!c_is_zero) {
+      TSM2X_CUDA(cudaMemcpy2DAsync(dC, ldd * eb, Cin, ldc * eb, m * eb, n, cudaMemcpyHostToDevice, hc->h2d));
+      TSM2X_CUDA(cudaEventRecord(b_ready, hc->h2d));
+      TSM2X_CUDA(cudaStreamWaitEvent(hc->comp, b_ready, 0));
+    }
     int64_t sw = std::max<int64_t>(1, (int64_t)(slab_target / ((size_t)ldd * eb)));
     sw = std::min<int64_t>(sw, k);
     const int64_t nslab = (k + sw - 1) / sw;
     const int nbuf = (int)std::min<int64_t>(3, nslab);
-    std::vector<T*> dA(nbuf);
-    std::vector<cudaEvent_t> loaded(nbuf), consumed(nbuf);
+    T* dA[3];
+    cudaEvent_t loaded[3], consumed[3];
     for (int i = 0; i < nbuf; ++i) {
-      TSM2X_TRY(hr.dmalloc((void**)&dA[i], (size_t)ldd * sw * eb));
-      TSM2X_TRY(hr.event(&loaded[i]));
-      TSM2X_TRY(hr.event(&consumed[i]));
+      TSM2X_TRY(hc->dbuf(std::string("A") + char('0' + i), (size_t)ldd * sw * eb, (void**)&dA[i]));
+      TSM2X_TRY(hc->event(&loaded[i]));
+      TSM2X_TRY(hc->event(&consumed[i]));
     }
     Stager stg;
-    TSM2X_TRY(stg.init(&hr, pinnedA, (size_t)m * eb * sw, 2));
-    cudaEvent_t b_ready;
-    TSM2X_TRY(hr.event(&b_ready));
-    TSM2X_CUDA(cudaEventRecord(b_ready, hr.h2d));
-    TSM2X_CUDA(cudaStreamWaitEvent(hr.comp, b_ready, 0));
+    TSM2X_TRY(stg.init(hc, pinnedA, (size_t)m * eb * sw, "stageA"));
     for (int64_t j = 0; j < nslab; ++j) {
       const int b = (int)(j % nbuf);
       const int64_t c0 = j * sw, cw = std::min(sw, k - c0);
-      if (j >= nbuf) TSM2X_CUDA(cudaStreamWaitEvent(hr.h2d, consumed[b], 0));
-      TSM2X_TRY(stg.copy(dA[b], ldd * eb, A + c0 * lda, lda * eb, m * eb, cw, hr.h2d));
-      TSM2X_CUDA(cudaEventRecord(loaded[b], hr.h2d));
-      TSM2X_CUDA(cudaStreamWaitEvent(hr.comp, loaded[b], 0));
-      uint32_t f = (c_is_zero && j == 0) ? TSM2X_FLAG_C_IS_ZERO : 0;
-      TSM2X_TRY(run_device<T>(variant == TSM2X_L_OPT2 ? TSM2X_L_OPT1 : variant, m, cw, n, dA[b], ldd, dB + c0, k, dC,
-                              ldd, params, f, TSM2X_IMPL_AUTO, hr.comp));
-      TSM2X_CUDA(cudaEventRecord(consumed[b], hr.comp));
+      if (j >= nbuf) TSM2X_CUDA(cudaStreamWaitEvent(hc->h2d, consumed[b], 0));
+      TSM2X_TRY(stg.copy(dA[b], ldd * eb, A + c0 * lda, lda * eb, m * eb, cw, hc->h2d));
+      TSM2X_CUDA(cudaEventRecord(loaded[b], hc->h2d));
+      TSM2X_CUDA(cudaStreamWaitEvent(hc->comp, loaded[b], 0));
+      const uint32_t f = (c_is_zero && j == 0) ? TSM2X_FLAG_C_IS_ZERO : 0;
+      TSM2X_TRY(run_device<T>(dev_variant, m, cw, n, dA[b], ldd, dB + c0, k, dC, ldd, params, f, TSM2X_IMPL_AUTO,
+                              hc->comp));
+      TSM2X_CUDA(cudaEventRecord(consumed[b], hc->comp));
     }
-    TSM2X_CUDA(cudaMemcpy2DAsync(Cout, ldc * eb, dC, ldd * eb, m * eb, n, cudaMemcpyDeviceToHost, hr.comp));
-    TSM2X_CUDA(cudaStreamSynchronize(hr.comp));
+    TSM2X_CUDA(cudaMemcpy2DAsync(Cout, ldc * eb, dC, ldd * eb, m * eb, n, cudaMemcpyDeviceToHost, hc->comp));
+    TSM2X_CUDA(cudaStreamSynchronize(hc->comp));
     return TSM2X_OK;
   }
 
-  // ---- TSM2L: row slabs of A and C
+  // ---- TSM2L: row slabs of A (and C); H2D / kernel / D2H on three streams
   const size_t row_bytes = (size_t)(k + (c_is_zero ? 0 : n)) * eb;
   int64_t rs = std::max<int64_t>(1024, (int64_t)(slab_target / std::max<size_t>(row_bytes, 1)));
   rs = (int64_t)align_up((size_t)std::min<int64_t>(rs, m), 32);
   const int64_t nslab = (m + rs - 1) / rs;
   const int nbuf = (int)std::min<int64_t>(3, nslab);
-  std::vector<T*> dA(nbuf), dC(nbuf);
-  std::vector<cudaEvent_t> loaded(nbuf), computed(nbuf), drained(nbuf);
+  T *dA[3], *dC[3];
+  cudaEvent_t loaded[3], computed[3], drained[3];
   for (int i = 0; i < nbuf; ++i) {
-    TSM2X_TRY(hr.dmalloc((void**)&dA[i], (size_t)rs * k * eb));
-    TSM2X_TRY(hr.dmalloc((void**)&dC[i], (size_t)rs * n * eb));
-    TSM2X_TRY(hr.event(&loaded[i]));
-    TSM2X_TRY(hr.event(&computed[i]));
-    TSM2X_TRY(hr.event(&drained[i]));
+    TSM2X_TRY(hc->dbuf(std::string("LA") + char('0' + i), (size_t)rs * k * eb, (void**)&dA[i]));
+    TSM2X_TRY(hc->dbuf(std::string("LC") + char('0' + i), (size_t)rs * n * eb, (void**)&dC[i]));
+    TSM2X_TRY(hc->event(&loaded[i]));
+    TSM2X_TRY(hc->event(&computed[i]));
+    TSM2X_TRY(hc->event(&drained[i]));
   }
-  Stager stg;
-  TSM2X_TRY(stg.init(&hr, pinnedA && (c_is_zero || is_pinned(Cin)), (size_t)rs * std::max<int64_t>(k, n) * eb, 2));
+  Stager stgA, stgC;
+  TSM2X_TRY(stgA.init(hc, pinnedA, (size_t)rs * k * eb, "stageLA"));
+  if (!c_is_zero) TSM2X_TRY(stgC.init(hc, is_pinned(Cin), (size_t)rs * n * eb, "stageLC"));
   const bool pinnedOut = is_pinned(Cout);
   T* out_stage[2] = {nullptr, nullptr};
   cudaEvent_t out_done[2];
   if (!pinnedOut) {
     for (int i = 0; i < 2; ++i) {
-      TSM2X_TRY(hr.hmalloc((void**)&out_stage[i], (size_t)rs * n * eb));
-      TSM2X_TRY(hr.event(&out_done[i]));
+      TSM2X_TRY(hc->hbuf(std::string("outL") + char('0' + i), (size_t)rs * n * eb, (void**)&out_stage[i]));
+      TSM2X_TRY(hc->event(&out_done[i]));
     }
   }
-  cudaEvent_t b_ready;
-  TSM2X_TRY(hr.event(&b_ready));
-  TSM2X_CUDA(cudaEventRecord(b_ready, hr.h2d));
-  TSM2X_CUDA(cudaStreamWaitEvent(hr.comp, b_ready, 0));
-  // pageable output: slab j's staged result is copied out once slab j+1 is enqueued
+  // pageable output: slab j's staged result is copied out while slab j+1 is in flight
   int64_t pend_r0 = -1, pend_rw = 0;
   int pend_i = 0;
-  auto flush_out = [&](void) -> int {
+  auto flush_out = [&]() -> int {
     if (pend_r0 < 0) return TSM2X_OK;
     TSM2X_CUDA(cudaEventSynchronize(out_done[pend_i]));
     par_copy2d(Cout + pend_r0, ldc * eb, out_stage[pend_i], pend_rw * eb, pend_rw * eb, n);
@@ -713,24 +785,23 @@ static int run_host_t(int variant, int64_t m, int64_t k, int64_t n, const T* A, 
   for (int64_t j = 0; j < nslab; ++j) {
     const int b = (int)(j % nbuf);
     const int64_t r0 = j * rs, rw = std::min(rs, m - r0);
-    if (j >= nbuf) TSM2X_CUDA(cudaStreamWaitEvent(hr.h2d, drained[b], 0));
-    TSM2X_TRY(stg.copy(dA[b], rs * eb, A + r0, lda * eb, rw * eb, k, hr.h2d));
-    if (!c_is_zero) TSM2X_TRY(stg.copy(dC[b], rs * eb, Cin + r0, ldc * eb, rw * eb, n, hr.h2d));
-    TSM2X_CUDA(cudaEventRecord(loaded[b], hr.h2d));
-    TSM2X_CUDA(cudaStreamWaitEvent(hr.comp, loaded[b], 0));
-    TSM2X_TRY(run_device<T>(TSM2X_L_OPT1, rw, k, n, dA[b], rs, dB, k, dC[b], rs, params,
-                            c_is_zero ? TSM2X_FLAG_C_IS_ZERO : 0, TSM2X_IMPL_AUTO, hr.comp));
-    TSM2X_CUDA(cudaEventRecord(computed[b], hr.comp));
-    TSM2X_CUDA(cudaStreamWaitEvent(hr.d2h, computed[b], 0));
+    if (j >= nbuf) TSM2X_CUDA(cudaStreamWaitEvent(hc->h2d, drained[b], 0));
+    TSM2X_TRY(stgA.copy(dA[b], rs * eb, A + r0, lda * eb, rw * eb, k, hc->h2d));
+    if (!c_is_zero) TSM2X_TRY(stgC.copy(dC[b], rs * eb, Cin + r0, ldc * eb, rw * eb, n, hc->h2d));
+    TSM2X_CUDA(cudaEventRecord(loaded[b], hc->h2d));
+    TSM2X_CUDA(cudaStreamWaitEvent(hc->comp, loaded[b], 0));
+    TSM2X_TRY(run_device<T>(dev_variant, rw, k, n, dA[b], rs, dB, k, dC[b], rs, params,
+                            c_is_zero ? TSM2X_FLAG_C_IS_ZERO : 0, TSM2X_IMPL_AUTO, hc->comp));
+    TSM2X_CUDA(cudaEventRecord(computed[b], hc->comp));
+    TSM2X_CUDA(cudaStreamWaitEvent(hc->d2h, computed[b], 0));
     if (pinnedOut) {
-      TSM2X_CUDA(cudaMemcpy2DAsync(Cout + r0, ldc * eb, dC[b], rs * eb, rw * eb, n, cudaMemcpyDeviceToHost, hr.d2h));
-      TSM2X_CUDA(cudaEventRecord(drained[b], hr.d2h));
+      TSM2X_CUDA(cudaMemcpy2DAsync(Cout + r0, ldc * eb, dC[b], rs * eb, rw * eb, n, cudaMemcpyDeviceToHost, hc->d2h));
+      TSM2X_CUDA(cudaEventRecord(drained[b], hc->d2h));
     } else {
       const int oi = (int)(j % 2);
-      if (pend_r0 >= 0 && pend_i == oi) TSM2X_TRY(flush_out());
-      TSM2X_CUDA(cudaMemcpy2DAsync(out_stage[oi], rw * eb, dC[b], rs * eb, rw * eb, n, cudaMemcpyDeviceToHost, hr.d2h));
-      TSM2X_CUDA(cudaEventRecord(drained[b], hr.d2h));
-      TSM2X_CUDA(cudaEventRecord(out_done[oi], hr.d2h));
+      TSM2X_CUDA(cudaMemcpy2DAsync(out_stage[oi], rw * eb, dC[b], rs * eb, rw * eb, n, cudaMemcpyDeviceToHost, hc->d2h));
+      TSM2X_CUDA(cudaEventRecord(drained[b], hc->d2h));
+      TSM2X_CUDA(cudaEventRecord(out_done[oi], hc->d2h));
       TSM2X_TRY(flush_out());
       pend_r0 = r0;
       pend_rw = rw;
@@ -738,8 +809,8 @@ static int run_host_t(int variant, int64_t m, int64_t k, int64_t n, const T* A, 
     }
   }
   TSM2X_TRY(flush_out());
-  TSM2X_CUDA(cudaStreamSynchronize(hr.d2h));
-  TSM2X_CUDA(cudaStreamSynchronize(hr.comp));
+  TSM2X_CUDA(cudaStreamSynchronize(hc->d2h));
+  TSM2X_CUDA(cudaStreamSynchronize(hc->comp));
   return TSM2X_OK;
 }
 

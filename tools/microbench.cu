@@ -142,6 +142,39 @@ __global__ void dmma_peak(double* out, int iters) {
   if (s == 1.2345) *out = s;
 }
 
+// half the warps DMMA, half DFMA: do the two share the FP64 datapath?
+__global__ void mixed_fp64_peak(double* out, int iters) {
+  const int w = threadIdx.x / 32;
+  double s = 0;
+  if (w & 1) {
+    double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+    double d[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { d[j][0] = j; d[j][1] = -j; }
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(d[j][0]), "+d"(d[j][1]) : "d"(a), "d"(b));
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += d[j][0] + d[j][1];
+  } else {
+    double a[8], b = 1.0000001, c = 0.9999999;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = threadIdx.x + j;
+    // DFMA warps do 8x the iterations' worth of lanes-FMAs to match DMMA work per warp: one DMMA
+    // (256 FMA) == 8 warp-DFMAs (32 FMA each)
+    for (int i = 0; i < iters * 8; ++i) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = fma(a[j], b, c);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += a[j];
+  }
+  if (s == 1.2345) *out = s;
+}
+
 static float time_kernel(void (*launch)(), int reps) {
   cudaEvent_t a, b; CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
   launch(); CK(cudaDeviceSynchronize());
@@ -207,6 +240,11 @@ int main(int argc, char** argv) {
     float ms = time_kernel([] { dmma_peak<<<g_grid, g_block>>>((double*)g_fp, g_iters); }, 5);
     double fl = double(g_grid) * (g_block / 32) * g_iters * 8 * 256 * 2;
     printf("{\"test\": \"dmma_m8n8k4_peak\", \"TFLOPs\": %.2f}\n", fl / ms / 1e9);
+  }
+  {
+    float ms = time_kernel([] { mixed_fp64_peak<<<g_grid, g_block>>>((double*)g_fp, g_iters); }, 5);
+    double fl = double(g_grid) * (g_block / 32) * g_iters * 8 * 256 * 2;  // both halves do the same FMAs
+    printf("{\"test\": \"mixed_dmma_dfma_peak\", \"TFLOPs\": %.2f}\n", fl / ms / 1e9);
   }
   {
     float ms = time_kernel([] { ffma_peak<<<g_grid, g_block>>>((float*)g_fp, g_iters); }, 5);
