@@ -64,6 +64,8 @@ typedef struct tsm2x_params {
 #define TSM2X_FLAG_C_IS_ZERO 0x1u   /* caller guarantees C == 0: C is written, never read  */
 #define TSM2X_FLAG_CHECK_ZERO_C 0x2u/* tsm2x_run + L_OPT2: verify C == 0 on the device
                                        (synchronises the stream); EINVAL if not          */
+#define TSM2X_FLAG_DETERMINISTIC 0x4u/* bitwise run-to-run reproducible combine (static split,
+                                       fixed-order sums); default: dynamic, fp64 atomics  */
 
 /* Kernel implementation override (tsm2x_run_ex); AUTO uses the B200 tuning table. */
 enum tsm2x_impl {

@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtsm2x.so")
 
 OK, EINVAL, ECUDA, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4
-FLAG_C_IS_ZERO, FLAG_CHECK_ZERO_C = 0x1, 0x2
+FLAG_C_IS_ZERO, FLAG_CHECK_ZERO_C, FLAG_DETERMINISTIC = 0x1, 0x2, 0x4
 IMPL = {"auto": 0, "ldg": 1, "tma": 2, "tsm2l": 3, "ablation": 4}
 SINGLE, DOUBLE = 0, 1
 

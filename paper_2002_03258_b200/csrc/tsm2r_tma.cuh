@@ -1,23 +1,27 @@
-// TSM2R stream kernel, TMA flavour (the production path on sm_100a).
+// TSM2R / TSM2L stream kernel, TMA flavour — the production path on sm_100a.
 //
-// Work decomposition. A (m x k, column-major) is cut into items = (row block of R rows,
-// column chunk of KCH columns). Items are handed out dynamically (one atomicAdd per item on a
-// global queue) in row-block-major order, so every SM keeps streaming until the queue is empty
-// whatever bandwidth it happens to get (per-SM DRAM bandwidth on B200 varies by ~+-10%, which a
-// static split turns straight into tail time — measured, profiles/README). Each item's partial
-// sum starts from zero and is written to its own slot; the last item of a row block to finish
-// adds the slots in chunk order plus C and writes C, then discards the slots from L2. The
-// result therefore does not depend on which CTA ran which item: the kernel is deterministic.
+// Work decomposition. A (m x k, column-major) is cut into items = (row block of R rows, column
+// chunk). Items are handed out dynamically (atomicAdd on a global queue), so every SM keeps
+// streaming until the queue is empty whatever DRAM bandwidth it happens to get: per-SM
+// bandwidth on B200 varies by ~10 %, which a static split turns straight into tail time
+// (profiles/README.md). Item sizes shrink towards the end of the queue — "big" chunks cover the
+// first ~80 % of every row block's columns and are dispatched first, "small" chunks the rest —
+// so the last items finish within ~10 us of each other. Row blocks split into several chunks
+// are combined by fire-and-forget fp64 reductions (red.global.add.f64) into C (fp64) or into
+// an fp64 accumulator (fp32, converted by tsm2_finalize). A row block that is a single chunk
+// (TSM2L shapes: k small) is written with plain vector stores — and, under the zero-C
+// contract, C is never read.
 //
 // Per CTA: warp 0 is the producer — one elected lane takes items off the queue and, per stage
 // of KC columns, issues 2-D TMA tensor loads of the A tile (R rows x KC columns as R/256 boxes
 // of 256 rows; rows >= m and columns >= k arrive zero-filled) plus a 1-D bulk copy of the KC
 // matching rows of Bt, completing on the stage's "full" mbarrier, and tags the stage with its
-// item id. Warps 1..CW are consumers: each thread owns RPT consecutive rows, reads its A vector
-// with one conflict-free LDS.128 per column and the Bt row as broadcast LDS.128s, and keeps the
-// NT outputs per row in registers; one lane per warp releases the stage on its "empty" mbarrier.
-// A STAGES-deep ring keeps ~(STAGES-1) * 32 KB of A in flight per SM independent of register
-// pressure — the B200 replacement for the paper's register double buffer (Alg 4).
+// item. Warps 1..CW are consumers: thread ct owns rows ct + 256*r (one per TMA box), reads them
+// with conflict-free LDS (32 consecutive elements per warp) and the Bt row as broadcast
+// LDS.128s, and keeps the NT outputs per row in registers; one lane per warp releases the stage on its "empty"
+// mbarrier. A STAGES-deep ring keeps ~(STAGES-1) * 32 KB of A in flight per SM independent of
+// register pressure — the B200 replacement for the paper's register double buffer (Alg 4,
+// PAPER.md:290-333) and of its t1 x t2 shared B tile (Alg 3).
 #pragma once
 #include <cuda.h>
 
@@ -41,7 +45,33 @@ struct TmaCfg {
   static constexpr int A_BYTES = A_ELEMS * (int)sizeof(T);
   static constexpr int B_BYTES = B_ELEMS * (int)sizeof(T);
   static constexpr int B_BYTES_PAD = (B_BYTES + 127) / 128 * 128;
-  static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES_PAD) + 2 * STAGES * 8 + STAGES * 8 + 16;
+  static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES_PAD) + 2 * STAGES * 8 + STAGES * 16 + 16;
+};
+
+// Item geometry: per row block, nbig chunks of kbig columns over [0, kbig_end), then nsmall
+// chunks of ksmall columns over [kbig_end, k). Ids: all big items (row-block major), then all
+// small items (row-block major). batch > 1 (single-chunk row blocks only) hands out that many
+// consecutive items per queue access.
+struct Items {
+  int64_t num_rb;
+  int64_t nbig, kbig, kbig_end;
+  int64_t nsmall, ksmall;
+  int64_t total;
+  int64_t batch;
+  __host__ __device__ int64_t nch() const { return nbig + nsmall; }
+  __device__ void decode(int64_t id, int64_t k, int64_t* rb, int64_t* c0, int64_t* c1) const {
+    const int64_t n_big_items = num_rb * nbig;
+    if (id < n_big_items) {
+      *rb = id / nbig;
+      *c0 = (id - *rb * nbig) * kbig;
+      *c1 = min64(*c0 + kbig, kbig_end);
+    } else {
+      const int64_t j = id - n_big_items;
+      *rb = j / nsmall;
+      *c0 = kbig_end + (j - *rb * nsmall) * ksmall;
+      *c1 = min64(*c0 + ksmall, k);
+    }
+  }
 };
 
 template <typename T>
@@ -51,15 +81,12 @@ struct DynArgs {
   int64_t ldc;
   int64_t m, k;
   int w;            // valid columns in this pass (<= NT)
-  int c_is_zero;
-  int64_t num_rb;
-  int64_t nch;      // column chunks per row block
-  int64_t kch;      // columns per chunk (multiple of KC)
-  int64_t items;    // num_rb * nch
-  int defer;        // 1: leave partials for reduce_items (very many chunks per row block)
-  T* ws;            // partial slots [items][NT][R]
-  int* counters;    // [num_rb] arrivals, zero between launches
-  int* queue;       // [0] next item, [1] producers finished; zero between launches
+  int c_is_zero;    // single-chunk row blocks: C is written, never read
+  int vec_c;        // C columns 16-B aligned (vector stores allowed)
+  double* acc;      // split row blocks, fp32: fp64 accumulator [NT][ldacc] (zeroed); fp64: null (C)
+  int64_t ldacc;
+  Items it;
+  unsigned long long* queue;  // [0] next item, [1] low 32 bits: producers finished
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
@@ -71,8 +98,8 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-__device__ __forceinline__ void discard_l2_line(const void* p) {
-  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+__device__ __forceinline__ void red_add(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
 struct ConsumerSync {
@@ -81,89 +108,239 @@ struct ConsumerSync {
   }
 };
 
-// Epilogue of one item (all consumer threads): direct C update when the row block is a single
-// chunk, else partial slot + arrival count; the last arrival combines the row block.
+// Epilogue of one item. Consumer thread ct owns rows ct + 256*r (r < RPT) of the row block, so
+// every warp-wide access below touches 32 consecutive elements of a C column: coalesced stores
+// for single-chunk row blocks (C (+)= acc), coalesced fp64 reductions for split row blocks
+// (into C for fp64, into the fp64 accumulator for fp32).
 template <typename T, int NT, int RPT, int R>
-__device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t item, int ct, T (&acc)[RPT][NT],
-                                            int* s_flag) {
-  const int64_t rb = item / a.nch;
-  const int lrow = ct * RPT;
-  const int64_t row0 = rb * R + lrow;
-  auto store = [&](const T (&v)[RPT][NT]) {
+__device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int ct, const T (&acc)[RPT][NT]) {
+  const int64_t row_base = rb * R + ct;
+  if (a.it.nch() == 1) {
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
-      if (j < a.w) {
-        T* cj = a.C + j * a.ldc;
+      if (j >= a.w) continue;
+      T* cj = a.C + j * a.ldc;
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          const int64_t row = row0 + r;
-          if (row < a.m) cj[row] = a.c_is_zero ? v[r][j] : cj[row] + v[r][j];
+      for (int r = 0; r < RPT; ++r) {
+        const int64_t row = row_base + r * TmaCfg<T, NT>::BOX;
+        if (row < a.m) {
+          if (a.c_is_zero)
+            __stcs(cj + row, acc[r][j]);
+          else
+            __stcs(cj + row, __ldcs(cj + row) + acc[r][j]);
         }
       }
     }
-  };
-  if (a.nch == 1) {
-    store(acc);
     return;
   }
-  using V = typename Vec<T>::type;
-  T* slot = a.ws + item * (int64_t)(NT * R);
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
-    T tmp[RPT];
+    if (j >= a.w) continue;
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) tmp[r] = acc[r][j];
-    *reinterpret_cast<V*>(slot + j * R + lrow) = vmake<T>(tmp);
+    for (int r = 0; r < RPT; ++r) {
+      const int64_t row = row_base + r * TmaCfg<T, NT>::BOX;
+      if constexpr (sizeof(T) == 8) {
+        if (row < a.m) red_add(reinterpret_cast<double*>(a.C) + j * a.ldc + row, (double)acc[r][j]);
+      } else {
+        red_add(a.acc + j * a.ldacc + row, (double)acc[r][j]);  // accumulator padded to whole row blocks
+      }
+    }
   }
-  if (a.defer) return;
-  __threadfence();
-  ConsumerSync()();
-  if (ct == 0) {
-    const int prev = atomicAdd(a.counters + rb, 1);
-    *s_flag = (prev == (int)(a.nch - 1));
+}
+
+// ------------------------------------------------------------------------------------------
+// Consumer policies: how one stage (R rows x KC columns of A in smem, the matching Bt rows) is
+// folded into the per-thread accumulators, and how an item's accumulators leave the CTA.
+
+// FMA: thread ct owns rows ct + 256*r; one scalar LDS per row per column (32 consecutive
+// elements per warp, conflict-free), Bt row as broadcast LDS.128s, NT FMAs per row per column.
+template <typename T, int NT>
+struct FmaConsumer {
+  using Cfg = TmaCfg<T, NT>;
+  using V = typename Vec<T>::type;
+  static constexpr int RPT = Cfg::RPT;
+  static constexpr bool kFragB = false;
+  T acc[RPT][NT];
+  int ct;
+  __device__ __forceinline__ void init(int consumer_thread) {
+    ct = consumer_thread;
+    zero();
   }
-  ConsumerSync()();
-  if (*s_flag) {
-    __threadfence();
-    T tot[RPT][NT];
+  __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int r = 0; r < RPT; ++r)
 #pragma unroll
-      for (int j = 0; j < NT; ++j) tot[r][j] = T(0);
-    const T* base = a.ws + rb * a.nch * (int64_t)(NT * R);
-    for (int64_t c = 0; c < a.nch; ++c) {
-      const T* p = base + c * (NT * R);
+      for (int j = 0; j < NT; ++j) acc[r][j] = T(0);
+  }
+  __device__ __forceinline__ void stage(const T* sA, const T* sB) {
+    const T* As = sA + ct;
 #pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        const V v = __ldcg(reinterpret_cast<const V*>(p + j * R + lrow));
+    for (int cc = 0; cc < Cfg::KC; ++cc) {
+      T av[RPT];
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) tot[r][j] += vget<T>(v, r);
+      for (int r = 0; r < RPT; ++r) av[r] = As[r * (Cfg::BOX * Cfg::KC) + cc * Cfg::BOX];
+      T b[NT];
+      if constexpr (NT * sizeof(T) >= 16) {
+        constexpr int PER = 16 / (int)sizeof(T);
+#pragma unroll
+        for (int i = 0; i < NT / PER; ++i) {
+          const V bv = reinterpret_cast<const V*>(sB + cc * NT)[i];
+#pragma unroll
+          for (int e = 0; e < PER; ++e) b[i * PER + e] = vget<T>(bv, e);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NT; ++i) b[i] = sB[cc * NT + i];
+      }
+#pragma unroll
+      for (int r = 0; r < RPT; ++r)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) acc[r][j] = fma(av[r], b[j], acc[r][j]);
+    }
+  }
+  __device__ __forceinline__ void finish(const DynArgs<T>& a, int64_t rb) const {
+    finish_item<T, NT, RPT, Cfg::R>(a, rb, ct, acc);
+  }
+};
+
+// FFMA2 (fp32): as FmaConsumer, but output columns are processed in pairs with the packed
+// fma.rn.f32x2 (one issue slot per two FMAs; the FP32 pipe, not issue, bounds n = 16).
+template <int NT>
+struct Ffma2Consumer {
+  using Cfg = TmaCfg<float, NT>;
+  static constexpr int RPT = Cfg::RPT;
+  static constexpr bool kFragB = false;
+  static_assert(NT % 2 == 0, "pairs of columns");
+  unsigned long long acc[RPT][NT / 2];  // packed (col 2p, col 2p+1)
+  int ct;
+  __device__ __forceinline__ void init(int consumer_thread) {
+    ct = consumer_thread;
+    zero();
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int p = 0; p < NT / 2; ++p) acc[r][p] = 0ull;
+  }
+  __device__ __forceinline__ void stage(const float* sA, const float* sB) {
+    const float* As = sA + ct;
+#pragma unroll
+    for (int cc = 0; cc < Cfg::KC; ++cc) {
+      unsigned long long a2[RPT];
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const float av = As[r * (Cfg::BOX * Cfg::KC) + cc * Cfg::BOX];
+        asm("mov.b64 %0, {%1, %1};" : "=l"(a2[r]) : "f"(av));
+      }
+      unsigned long long b2[NT / 2];
+      const unsigned long long* bp = reinterpret_cast<const unsigned long long*>(sB + cc * NT);
+#pragma unroll
+      for (int p = 0; p < NT / 2; ++p) b2[p] = bp[p];
+#pragma unroll
+      for (int r = 0; r < RPT; ++r)
+#pragma unroll
+        for (int p = 0; p < NT / 2; ++p) asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[r][p]) : "l"(a2[r]), "l"(b2[p]));
+    }
+  }
+  __device__ __forceinline__ void finish(const DynArgs<float>& a, int64_t rb) const {
+    float out[RPT][NT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int p = 0; p < NT / 2; ++p) asm("mov.b64 {%0, %1}, %2;" : "=f"(out[r][2 * p]), "=f"(out[r][2 * p + 1]) : "l"(acc[r][p]));
+    finish_item<float, NT, RPT, Cfg::R>(a, rb, ct, out);
+  }
+};
+
+// DMMA (fp64, NT in {8, 16}): the FP64 tensor-core MMA m8n8k4 (DMMA.8x8x4). Warp w owns rows
+// [64w, 64w+64) of the row block as four 16-row groups; one LDS.128 per lane loads rows
+// (2g, 2g+1) of column t of a group — two A fragments (M tiles of the even and the odd rows) for
+// 8 lanes x 4 columns, 4 conflict-free wavefronts. Bt is staged in fragment order (prep_bfrag)
+// so each B fragment is one LDS.64 per lane. 32 DMMAs per warp per stage replace 256 DFMAs and
+// 64 LDS.128 of the FMA consumer; the FP64 datapath is shared (measured), so this buys issue
+// slots and power, not peak.
+template <int NT>
+struct DmmaConsumer {
+  using Cfg = TmaCfg<double, NT>;
+  static constexpr bool kFragB = true;
+  static_assert(NT == 8 || NT == 16, "DMMA consumer needs NT in {8, 16}");
+  static constexpr int NTI = NT / 8;  // N tiles
+  double acc[4][2][NTI][2];           // [row group][M tile (even/odd rows)][N tile][2 columns]
+  int warp, lane;
+  __device__ __forceinline__ void init(int consumer_thread) {
+    warp = consumer_thread / 32;
+    lane = consumer_thread % 32;
+    zero();
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt) acc[q][mt][nt][0] = acc[q][mt][nt][1] = 0.0;
+  }
+  __device__ __forceinline__ void stage(const double* sA, const double* sB) {
+    const int g = lane >> 2, t = lane & 3;
+    // box = warp / 4, rows within the box start at 64 * (warp % 4)
+    const double* As = sA + (warp >> 2) * (Cfg::BOX * Cfg::KC) + (64 * (warp & 3) + 2 * g);
+#pragma unroll
+    for (int ks = 0; ks < Cfg::KC / 4; ++ks) {
+      double b[NTI];
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt) b[nt] = sB[(ks * NTI + nt) * 32 + lane];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 av = *reinterpret_cast<const double2*>(As + (4 * ks + t) * Cfg::BOX + 16 * q);
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt) {
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[q][0][nt][0]), "+d"(acc[q][0][nt][1]) : "d"(av.x), "d"(b[nt]));
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[q][1][nt][0]), "+d"(acc[q][1][nt][1]) : "d"(av.y), "d"(b[nt]));
+        }
       }
     }
-    store(tot);
-    ConsumerSync()();  // everyone has read the slots
-    // the slots are dead: drop them from L2 without a DRAM write-back
-    const int64_t lines = a.nch * (int64_t)(NT * R * sizeof(T)) / 128;
-    const char* b = reinterpret_cast<const char*>(base);
-    for (int64_t l = ct; l < lines; l += TmaCfg<T, NT>::CW * 32) discard_l2_line(b + l * 128);
-    if (ct == 0) a.counters[rb] = 0;  // ready for the next launch on this workspace
   }
-  ConsumerSync()();  // s_flag reuse
-}
+  // accumulator (q, mt, nt, e) holds row 64w + 16q + 2g + mt, column 8nt + 2t + e
+  __device__ __forceinline__ void finish(const DynArgs<double>& a, int64_t rb) const {
+    const int g = lane >> 2, t = lane & 3;
+    const int64_t base = rb * Cfg::R + 64 * warp + 2 * g;
+    const bool split = a.it.nch() > 1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int64_t row = base + 16 * q + mt;
+        if (row >= a.m) continue;
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = 8 * nt + 2 * t + e;
+            if (j >= a.w) continue;
+            double* c = a.C + j * a.ldc + row;
+            if (split)
+              red_add(c, acc[q][mt][nt][e]);
+            else
+              *c = a.c_is_zero ? acc[q][mt][nt][e] : *c + acc[q][mt][nt][e];
+          }
+      }
+  }
+};
 
-template <typename T, int NT>
+template <typename T, int NT, typename Consumer>
 __global__ void __launch_bounds__(TmaCfg<T, NT>::THREADS, 1)
     tsm2r_stream_tma(const DynArgs<T> a, const __grid_constant__ CUtensorMap tmA) {
   using Cfg = TmaCfg<T, NT>;
-  using V = typename Vec<T>::type;
-  constexpr int RPT = Cfg::RPT, R = Cfg::R, KC = Cfg::KC, STAGES = Cfg::STAGES;
+  constexpr int R = Cfg::R, KC = Cfg::KC, STAGES = Cfg::STAGES;
   extern __shared__ __align__(1024) unsigned char smem[];
   T* sA = reinterpret_cast<T*>(smem);
   T* sB = reinterpret_cast<T*>(smem + STAGES * Cfg::A_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * (Cfg::A_BYTES + Cfg::B_BYTES_PAD));
   uint64_t* empty = full + STAGES;
-  int64_t* meta = reinterpret_cast<int64_t*>(empty + STAGES);  // item id of each stage, -1 = end
-  int* s_flag = reinterpret_cast<int*>(meta + STAGES);
+  longlong2* meta = reinterpret_cast<longlong2*>(empty + STAGES);  // (row block, item id) per stage; id -1 = end
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
@@ -182,37 +359,39 @@ __global__ void __launch_bounds__(TmaCfg<T, NT>::THREADS, 1)
       const uint64_t pol = policy_evict_first();
       int it = 0;
       for (;;) {
-        const int64_t item = atomicAdd(reinterpret_cast<unsigned long long*>(a.queue), 1ull);
-        if (item >= a.items) break;
-        const int64_t rb = item / a.nch;
-        const int64_t col0 = (item - rb * a.nch) * a.kch;
-        const int64_t col1 = min64(a.k, col0 + a.kch);
-        const int64_t row_base = rb * R;
-        const int nbox = (int)min64(Cfg::NBOX, (a.m - row_base + Cfg::BOX - 1) / Cfg::BOX);
-        const uint32_t tx = (uint32_t)(nbox * Cfg::BOX * KC * (int)sizeof(T) + Cfg::B_BYTES);
-        for (int64_t col = col0; col < col1; col += KC, ++it) {
-          const int s = it % STAGES;
-          const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
-          mbar_wait(&empty[s], ph ^ 1u);
-          meta[s] = item;
-          mbar_arrive_expect_tx(&full[s], tx);
-          for (int b = 0; b < nbox; ++b)
-            tma_load_2d(sA + (size_t)s * Cfg::A_ELEMS + b * (Cfg::BOX * KC), &tmA, (int)(row_base + b * Cfg::BOX),
-                        (int)col, &full[s], pol);
-          bulk_g2s(sB + (size_t)s * (Cfg::B_BYTES_PAD / sizeof(T)), a.Bt + col * NT, Cfg::B_BYTES, &full[s]);
+        const int64_t first = (int64_t)atomicAdd(a.queue, (unsigned long long)a.it.batch);
+        if (first >= a.it.total) break;
+        const int64_t last = min64(first + a.it.batch, a.it.total);
+        for (int64_t item = first; item < last; ++item) {
+          int64_t rb, col0, col1;
+          a.it.decode(item, a.k, &rb, &col0, &col1);
+          const int64_t row_base = rb * R;
+          const int nbox = (int)min64(Cfg::NBOX, (a.m - row_base + Cfg::BOX - 1) / Cfg::BOX);
+          const uint32_t tx = (uint32_t)(nbox * Cfg::BOX * KC * (int)sizeof(T) + Cfg::B_BYTES);
+          for (int64_t col = col0; col < col1; col += KC, ++it) {
+            const int s = it % STAGES;
+            const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+            mbar_wait(&empty[s], ph ^ 1u);
+            meta[s] = make_longlong2(rb, item);
+            mbar_arrive_expect_tx(&full[s], tx);
+            for (int b = 0; b < nbox; ++b)
+              tma_load_2d(sA + (size_t)s * Cfg::A_ELEMS + b * (Cfg::BOX * KC), &tmA, (int)(row_base + b * Cfg::BOX),
+                          (int)col, &full[s], pol);
+            bulk_g2s(sB + (size_t)s * (Cfg::B_BYTES_PAD / sizeof(T)), a.Bt + col * NT, Cfg::B_BYTES, &full[s]);
+          }
         }
       }
       // end-of-work marker for the consumers
       const int s = it % STAGES;
       mbar_wait(&empty[s], ((uint32_t)(it / STAGES) & 1u) ^ 1u);
-      meta[s] = -1;
+      meta[s] = make_longlong2(-1, -1);
       mbar_arrive(&full[s]);
       // the last producer out resets the queue for the next launch on this workspace
       __threadfence();
-      const unsigned prev = atomicAdd(reinterpret_cast<unsigned*>(a.queue) + 2, 1u);
+      const unsigned prev = atomicAdd(reinterpret_cast<unsigned*>(a.queue + 1), 1u);
       if (prev == gridDim.x - 1) {
-        *reinterpret_cast<unsigned long long*>(a.queue) = 0ull;
-        reinterpret_cast<unsigned*>(a.queue)[2] = 0u;
+        a.queue[0] = 0ull;
+        a.queue[1] = 0ull;
         __threadfence();
       }
     }
@@ -220,75 +399,55 @@ __global__ void __launch_bounds__(TmaCfg<T, NT>::THREADS, 1)
   }
 
   // ---------------- consumers
-  const int ct = threadIdx.x - 32;
-  const int lrow = ct * RPT;
-  const int box = lrow / Cfg::BOX, rin = lrow % Cfg::BOX;
-  T acc[RPT][NT];
-#pragma unroll
-  for (int r = 0; r < RPT; ++r)
-#pragma unroll
-    for (int j = 0; j < NT; ++j) acc[r][j] = T(0);
-  int64_t cur = -1;
+  Consumer cons;
+  cons.init(threadIdx.x - 32);
+  int64_t cur = -1, cur_rb = 0;
   for (int it = 0;; ++it) {
     const int s = it % STAGES;
     const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
     mbar_wait(&full[s], ph);
-    const int64_t item = meta[s];
-    if (item != cur) {
+    const longlong2 md = meta[s];
+    if (md.y != cur) {
       if (cur >= 0) {
-        finish_item<T, NT, RPT, R>(a, cur, ct, acc, s_flag);
-#pragma unroll
-        for (int r = 0; r < RPT; ++r)
-#pragma unroll
-          for (int j = 0; j < NT; ++j) acc[r][j] = T(0);
+        cons.finish(a, cur_rb);
+        cons.zero();
       }
-      if (item < 0) break;
-      cur = item;
+      if (md.y < 0) break;
+      cur = md.y;
+      cur_rb = md.x;
     }
-    const T* As = sA + (size_t)s * Cfg::A_ELEMS + box * (Cfg::BOX * KC) + rin;
-    const T* Bs = sB + (size_t)s * (Cfg::B_BYTES_PAD / sizeof(T));
-#pragma unroll
-    for (int cc = 0; cc < KC; ++cc) {
-      const V av = *reinterpret_cast<const V*>(As + cc * Cfg::BOX);
-      T b[NT];
-      if constexpr (NT * sizeof(T) >= 16) {
-        constexpr int PER = 16 / (int)sizeof(T);
-#pragma unroll
-        for (int i = 0; i < NT / PER; ++i) {
-          const V bv = reinterpret_cast<const V*>(Bs + cc * NT)[i];
-#pragma unroll
-          for (int e = 0; e < PER; ++e) b[i * PER + e] = vget<T>(bv, e);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < NT; ++i) b[i] = Bs[cc * NT + i];
-      }
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        const T ar = vget<T>(av, r);
-#pragma unroll
-        for (int j = 0; j < NT; ++j) acc[r][j] = fma(ar, b[j], acc[r][j]);
-      }
-    }
+    cons.stage(sA + (size_t)s * Cfg::A_ELEMS, sB + (size_t)s * (Cfg::B_BYTES_PAD / sizeof(T)));
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 }
 
-// Combine for row blocks split into very many chunks (defer mode): one thread per (row, column),
-// slots summed in chunk order — the same order as finish_item, so the same bits.
-template <typename T, int NT, int R>
-__global__ void reduce_items(const DynArgs<T> a) {
-  const int lrow = blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t rb = blockIdx.y;
-  const int64_t row = rb * R + lrow;
-  if (lrow >= R || row >= a.m) return;
-  const T* base = a.ws + rb * a.nch * (int64_t)(NT * R);
-  for (int j = 0; j < a.w; ++j) {
-    T tot = T(0);
-    for (int64_t c = 0; c < a.nch; ++c) tot += base[c * (NT * R) + j * R + lrow];
-    T* cp = a.C + row + j * a.ldc;
-    *cp = a.c_is_zero ? tot : *cp + tot;
+// Bt in DMMA fragment order: for each group of 4 B rows (kg) and N tile (nt), the 32 values in
+// lane order, lane (g = lane/4, t = lane%4) holding B[4kg + t][8nt + g]; zero padded like prep_bt.
+template <int NT>
+__global__ void prep_bfrag(const double* __restrict__ B, int64_t ldb, int64_t k, int64_t kpad, int w,
+                           double* __restrict__ Bf) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= kpad * NT) return;
+  const int lane = (int)(i % 32);
+  const int64_t tile = i / 32;            // kg * (NT/8) + nt
+  const int nt = (int)(tile % (NT / 8));
+  const int64_t kg = tile / (NT / 8);
+  const int64_t row = 4 * kg + (lane & 3);
+  const int col = 8 * nt + (lane >> 2);
+  Bf[i] = (row < k && col < w) ? B[row + col * ldb] : 0.0;
+}
+
+// fp32 split row blocks: C = (float)((double)C + acc) (or (float)acc under the zero-C contract).
+template <typename T>
+__global__ void tsm2_finalize(const double* __restrict__ acc, int64_t ldacc, T* C, int64_t ldc, int64_t m, int w,
+                              int c_is_zero) {
+  const int64_t tot = m * w;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = i / m, r = i - j * m;
+    const double v = acc[j * ldacc + r];
+    T* c = C + j * ldc + r;
+    *c = c_is_zero ? (T)v : (T)((double)*c + v);
   }
 }
 

@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -22,6 +23,7 @@
 #include "tsm2l.cuh"
 #include "tsm2r_stream.cuh"
 #include "tsm2r_tma.cuh"
+#include "tsm2r_tma_static.cuh"
 
 namespace tsm2x {
 
@@ -245,27 +247,85 @@ static int run_ablation(int variant, int64_t m, int64_t k, int64_t n, const T* A
 
 // ---- TSM2R pass: C[:, p:p+w] (+)= A * B[:, p:p+w] -----------------------------------------
 // Bt (this pass of B, row-major, zero padded to kpad rows) at the front of the workspace.
+// frag = true: DMMA fragment order instead (prep_bfrag; fp64, NT in {8, 16}).
 template <typename T, int NT>
 static int stage_bt(Workspace* ws, int64_t k, int64_t kpad, int w, const T* B, int64_t ldb, size_t extra_bytes,
-                    size_t counters, cudaStream_t s, T** Bt, char** rest) {
+                    size_t counters, cudaStream_t s, T** Bt, char** rest, bool frag = false) {
   const size_t bt_bytes = align_up((size_t)kpad * NT * sizeof(T), 256);
   TSM2X_TRY(ws_reserve(ws, bt_bytes + extra_bytes, counters, s));
   *Bt = reinterpret_cast<T*>(ws->buf);
   *rest = static_cast<char*>(ws->buf) + bt_bytes;
   const int64_t tot = kpad * NT;
+  if constexpr (sizeof(T) == 8 && (NT == 8 || NT == 16)) {
+    if (frag) {
+      prep_bfrag<NT><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(B, ldb, k, kpad, w, *Bt);
+      return check_launch("prep_bfrag");
+    }
+  }
   prep_bt<T, NT><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(B, ldb, k, kpad, w, *Bt);
   return check_launch("prep_bt");
 }
 
-// TMA flavour: dynamic items, deterministic combine (tsm2r_tma.cuh)
+// Consumer choice (tsm2r_tma.cuh): DMMA for fp64 split row blocks at NT >= 8 (issue slots /
+// power at the FP64-heavy widths), packed FFMA2 for fp32 at NT >= 2, plain FMA otherwise.
+enum ConsumerKind { kFma = 0, kDmma = 1, kFfma2 = 2 };
+static int g_consumer_override = -1;  // TSM2X_CONSUMER=fma|dmma|ffma2 (ablation / benchmarks)
+
+template <typename T, int NT>
+static int pick_consumer(bool split) {
+  static const int env = [] {
+    const char* e = getenv("TSM2X_CONSUMER");
+    if (!e) return -1;
+    if (!strcmp(e, "fma")) return (int)kFma;
+    if (!strcmp(e, "dmma")) return (int)kDmma;
+    if (!strcmp(e, "ffma2")) return (int)kFfma2;
+    return -1;
+  }();
+  const int want = g_consumer_override >= 0 ? g_consumer_override : env;
+  const bool dmma_ok = sizeof(T) == 8 && (NT == 8 || NT == 16);
+  const bool ffma2_ok = sizeof(T) == 4 && NT >= 2;
+  if (want == kFma) return kFma;
+  if (want == kDmma) return dmma_ok ? kDmma : kFma;
+  if (want == kFfma2) return ffma2_ok ? kFfma2 : kFma;
+  if (dmma_ok && split) return kDmma;
+  if (ffma2_ok) return kFfma2;
+  return kFma;
+}
+
+template <typename T, int NT, int KIND>
+struct ConsumerFor {
+  using type = FmaConsumer<T, NT>;
+};
+template <int NT>
+struct ConsumerFor<double, NT, kDmma> {
+  using type = typename std::conditional<(NT == 8 || NT == 16), DmmaConsumer<(NT >= 8 ? NT : 8)>,
+                                         FmaConsumer<double, NT>>::type;
+};
+template <int NT>
+struct ConsumerFor<float, NT, kFfma2> {
+  using type = typename std::conditional<(NT >= 2), Ffma2Consumer<(NT >= 2 ? NT : 2)>, FmaConsumer<float, NT>>::type;
+};
+
+template <typename T, int NT, int KIND>
+static int launch_tma_kernel(const DynArgs<T>& a_in, const CUtensorMap& tmap_in, int64_t G, cudaStream_t s) {
+  using Cfg = TmaCfg<T, NT>;
+  using Cons = typename ConsumerFor<T, NT, KIND>::type;
+  auto kern = tsm2r_stream_tma<T, NT, Cons>;
+  TSM2X_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  DynArgs<T> a = a_in;
+  alignas(64) CUtensorMap tmap = tmap_in;
+  void* args[] = {&a, &tmap};
+  TSM2X_CUDA(cudaLaunchKernel((const void*)kern, dim3((unsigned)G), dim3(Cfg::THREADS), args, Cfg::SMEM, s));
+  return check_launch("tsm2r_stream_tma");
+}
+
+// TMA flavour, dynamic items (tsm2r_tma.cuh): item sizes from the per-CTA share of the work.
 template <typename T, int NT>
 static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k, int w, const T* A, int64_t lda,
                          const T* B, int64_t ldb, T* C, int64_t ldc, bool c_is_zero, cudaStream_t s) {
   using Cfg = TmaCfg<T, NT>;
-  auto kern = tsm2r_stream_tma<T, NT>;
-  TSM2X_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  const int occ = occupancy(kern, Cfg::THREADS, Cfg::SMEM);
-  const int64_t G_full = (int64_t)di.sms * occ;
+  const int64_t G_full = (int64_t)di.sms;  // one CTA per SM (smem-bound by design)
+  const size_t eb = sizeof(T);
   DynArgs<T> a;
   a.C = C;
   a.ldc = ldc;
@@ -273,42 +333,126 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   a.k = k;
   a.w = w;
   a.c_is_zero = c_is_zero ? 1 : 0;
-  a.num_rb = (m + Cfg::R - 1) / Cfg::R;
-  // ~24 items per CTA so the dynamic queue can even out per-SM bandwidth differences; chunks of
-  // at least 256 columns keep the partial-slot traffic (2*NT/kch of A's bytes, L2 only) small
-  const int64_t want_items = 24 * G_full;
-  int64_t nch = std::max<int64_t>(1, (want_items + a.num_rb - 1) / a.num_rb);
-  int64_t kch = (int64_t)align_up((size_t)((k + nch - 1) / nch), Cfg::KC);
-  kch = std::max<int64_t>(kch, std::min<int64_t>(256, (int64_t)align_up((size_t)k, Cfg::KC)));
-  a.kch = kch;
-  a.nch = (k + kch - 1) / kch;
-  a.items = a.num_rb * a.nch;
-  a.defer = a.nch > 128 ? 1 : 0;
-  const int64_t G = std::min<int64_t>(G_full, a.items);
+  a.vec_c = aligned16(C) && (ldc % Vec<T>::N == 0);
+  Items& it = a.it;
+  it.num_rb = (m + Cfg::R - 1) / Cfg::R;
+  const double col_bytes = (double)Cfg::R * eb;  // one column of one row block
+  const double total = (double)m * k * eb;
+  const double per_cta = total / (double)G_full;
+  const double small_b = std::min(512.0 * 1024, std::max(64.0 * 1024, per_cta / 48));
+  const double big_b = std::min(4.0 * 1024 * 1024, std::max(small_b, per_cta / 6));
+  const int64_t ksmall = std::max<int64_t>(Cfg::KC, (int64_t)align_up((size_t)(small_b / col_bytes), Cfg::KC));
+  const int64_t kbig = std::max<int64_t>(ksmall, (int64_t)align_up((size_t)(big_b / col_bytes), Cfg::KC));
+  if ((double)k * col_bytes <= 1024.0 * 1024 || k <= ksmall) {
+    // single-chunk row blocks (TSM2L shapes): no split, batched dispatch of ~1 MB per grab
+    it.nbig = 0;
+    it.kbig = Cfg::KC;
+    it.kbig_end = 0;
+    it.nsmall = 1;
+    it.ksmall = (int64_t)align_up((size_t)k, Cfg::KC);
+    it.batch = std::max<int64_t>(1, (int64_t)(1024.0 * 1024 / ((double)k * col_bytes)));
+  } else {
+    const int64_t tail = std::min<int64_t>(k, (int64_t)align_up((size_t)((k + 4) / 5), (size_t)ksmall));
+    it.kbig_end = ((k - tail) / Cfg::KC) * Cfg::KC;
+    it.kbig = kbig;
+    it.nbig = it.kbig_end > 0 ? (it.kbig_end + kbig - 1) / kbig : 0;
+    it.ksmall = ksmall;
+    it.nsmall = (k - it.kbig_end + ksmall - 1) / ksmall;
+    it.batch = 1;
+  }
+  it.total = it.num_rb * it.nch();
+  const int64_t G = std::min<int64_t>(G_full, (it.total + it.batch - 1) / it.batch);
+  const bool split = it.nch() > 1;
   const int64_t kpad = (int64_t)align_up((size_t)k, Cfg::KC);
-  const size_t slots = a.nch > 1 ? (size_t)a.items * NT * Cfg::R * sizeof(T) : 0;
+  a.ldacc = (int64_t)it.num_rb * Cfg::R;
+  const size_t acc_bytes = (split && sizeof(T) == 4) ? (size_t)a.ldacc * NT * sizeof(double) : 0;
+  const int kind = pick_consumer<T, NT>(split);
   T* Bt;
   char* rest;
-  TSM2X_TRY((stage_bt<T, NT>(ws, k, kpad, w, B, ldb, slots, (size_t)a.num_rb + 4, s, &Bt, &rest)));
+  TSM2X_TRY((stage_bt<T, NT>(ws, k, kpad, w, B, ldb, acc_bytes, 8, s, &Bt, &rest, kind == kDmma)));
+  a.Bt = Bt;
+  a.acc = acc_bytes ? reinterpret_cast<double*>(rest) : nullptr;
+  a.queue = reinterpret_cast<unsigned long long*>(ws->counters);  // zero between launches
+  if (split) {
+    if (sizeof(T) == 4) {
+      TSM2X_CUDA(cudaMemsetAsync(a.acc, 0, acc_bytes, s));
+    } else if (c_is_zero) {
+      TSM2X_CUDA(cudaMemset2DAsync(C, ldc * eb, 0, m * eb, w, s));
+    }
+  }
+  alignas(64) CUtensorMap tmap;
+  TSM2X_TRY(encode_a_map(&tmap, A, m, k, lda, eb, Cfg::BOX, Cfg::KC));
+  const bool timed = t_ev_start && t_ev_stop;
+  if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
+  if (kind == kDmma)
+    TSM2X_TRY((launch_tma_kernel<T, NT, kDmma>(a, tmap, G, s)));
+  else if (kind == kFfma2)
+    TSM2X_TRY((launch_tma_kernel<T, NT, kFfma2>(a, tmap, G, s)));
+  else
+    TSM2X_TRY((launch_tma_kernel<T, NT, kFma>(a, tmap, G, s)));
+  if (timed) {
+    TSM2X_CUDA(cudaEventRecord(t_ev_stop, s));
+    t_ev_start = t_ev_stop = nullptr;
+  }
+  if (split && sizeof(T) == 4) {
+    const int64_t tot = m * w;
+    const unsigned grid = (unsigned)std::min<int64_t>((tot + 255) / 256, (int64_t)di.sms * 8);
+    tsm2_finalize<T><<<grid, 256, 0, s>>>(a.acc, a.ldacc, C, ldc, m, w, a.c_is_zero);
+    TSM2X_TRY(check_launch("tsm2_finalize"));
+  }
+  return TSM2X_OK;
+}
+
+// TMA flavour, static stream-K with fixed-order combine (tsm2r_tma_static.cuh): deterministic.
+template <typename T, int NT>
+static int run_tsm2r_tma_static(const DevInfo& di, Workspace* ws, int64_t m, int64_t k, int w, const T* A,
+                                int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc, bool c_is_zero,
+                                cudaStream_t s) {
+  using Cfg = TmaCfg<T, NT>;
+  auto kern = tsm2r_static_tma<T, NT>;
+  TSM2X_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  const int occ = occupancy(kern, Cfg::THREADS, Cfg::SMEM);
+  StreamArgs<T> a;
+  a.A = A;
+  a.lda = lda;
+  a.C = C;
+  a.ldc = ldc;
+  a.m = m;
+  a.k = k;
+  a.w = w;
+  a.c_is_zero = c_is_zero ? 1 : 0;
+  a.num_rb = (m + Cfg::R - 1) / Cfg::R;
+  a.KC = Cfg::KC;
+  const int64_t num_kb = (k + Cfg::KC - 1) / Cfg::KC;
+  const int64_t units = a.num_rb * num_kb;
+  const int64_t G = std::min<int64_t>(units, (int64_t)di.sms * occ);
+  a.part.units = units;
+  a.part.num_kb = num_kb;
+  a.part.G = G;
+  const int64_t max_contrib = (num_kb * G + units - 1) / units + 1;
+  a.defer = (max_contrib > 24) ? 1 : 0;
+  const size_t part_bytes = (size_t)G * 2 * NT * Cfg::R * sizeof(T);
+  T* Bt;
+  char* rest;
+  TSM2X_TRY((stage_bt<T, NT>(ws, k, num_kb * Cfg::KC, w, B, ldb, part_bytes, (size_t)a.num_rb + 4, s, &Bt, &rest)));
   a.Bt = Bt;
   a.ws = reinterpret_cast<T*>(rest);
-  a.queue = ws->counters;          // [0..1] 64-bit item counter, [2] producers finished
-  a.counters = ws->counters + 4;   // per row block arrivals
+  a.counters = ws->counters + 4;
   alignas(64) CUtensorMap tmap;
   TSM2X_TRY(encode_a_map(&tmap, A, m, k, lda, sizeof(T), Cfg::BOX, Cfg::KC));
   const bool timed = t_ev_start && t_ev_stop;
   if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
   void* args[] = {&a, &tmap};
   TSM2X_CUDA(cudaLaunchKernel((const void*)kern, dim3((unsigned)G), dim3(Cfg::THREADS), args, Cfg::SMEM, s));
-  TSM2X_TRY(check_launch("tsm2r_stream_tma"));
+  TSM2X_TRY(check_launch("tsm2r_static_tma"));
   if (timed) {
     TSM2X_CUDA(cudaEventRecord(t_ev_stop, s));
     t_ev_start = t_ev_stop = nullptr;
   }
   if (a.defer) {
     dim3 grid((unsigned)((Cfg::R + 255) / 256), (unsigned)a.num_rb);
-    reduce_items<T, NT, Cfg::R><<<grid, 256, 0, s>>>(a);
-    TSM2X_TRY(check_launch("reduce_items"));
+    reduce_partials<T, NT, Cfg::R><<<grid, 256, 0, s>>>(a);
+    TSM2X_TRY(check_launch("reduce_partials"));
   }
   return TSM2X_OK;
 }
@@ -381,11 +525,13 @@ static int run_tsm2r_ldg(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
 
 template <typename T, int NT>
 static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m, int64_t k, int w, const T* A,
-                          int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc, bool c_is_zero, cudaStream_t s) {
+                          int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc, bool c_is_zero, bool deterministic,
+                          cudaStream_t s) {
   // TMA needs 16-byte aligned base and column stride; coordinates are int32
   const bool tma_ok = aligned16(A) && ((lda * (int64_t)sizeof(T)) % 16 == 0) && m < (int64_t(1) << 31) &&
                       k < (int64_t(1) << 31);
   const bool tma = (impl == TSM2X_IMPL_AUTO || impl == TSM2X_IMPL_STREAM_TMA) && tma_ok;
+  if (tma && deterministic) return run_tsm2r_tma_static<T, NT>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, s);
   if (tma) return run_tsm2r_tma<T, NT>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, s);
   return run_tsm2r_ldg<T, NT>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, s);
 }
@@ -477,7 +623,11 @@ static int run_device(int variant, int64_t m, int64_t k, int64_t n, const T* A, 
     if (variant > TSM2X_V2) impl = TSM2X_IMPL_AUTO;
     else return run_ablation<T>(variant, m, k, n, A, lda, B, ldb, C, ldc, params, c_is_zero, s);
   }
-  const bool use_l = (impl == TSM2X_IMPL_TSM2L) || (impl == TSM2X_IMPL_AUTO && k <= TSM2L_KMAX);
+  const bool determ = (flags & TSM2X_FLAG_DETERMINISTIC) != 0;
+  // the TMA stream kernel also covers TSM2L shapes (single-chunk row blocks); the LDG TSM2L
+  // kernel is the fallback for layouts TMA cannot describe, or on request
+  const bool tma_layout = aligned16(A) && ((lda * (int64_t)sizeof(T)) % 16 == 0);
+  const bool use_l = (impl == TSM2X_IMPL_TSM2L) || (impl == TSM2X_IMPL_AUTO && k <= TSM2L_KMAX && !tma_layout);
   if (use_l && k > TSM2L_KMAX) return fail(TSM2X_EINVAL, "TSM2L kernel needs k <= %d, got %lld", TSM2L_KMAX, (long long)k);
   for (int64_t p = 0; p < n; p += 16) {
     const int w = (int)std::min<int64_t>(16, n - p);
@@ -488,7 +638,7 @@ static int run_device(int variant, int64_t m, int64_t k, int64_t n, const T* A, 
 #define TSM2X_PASS(NTV)                                                                                     \
   case NTV:                                                                                                 \
     rc = use_l ? run_tsm2l_pass<T, NTV>(di, m, k, w, A, lda, Bp, ldb, Cp, ldc, c_is_zero, s)                \
-               : run_tsm2r_pass<T, NTV>(di, ws, impl, m, k, w, A, lda, Bp, ldb, Cp, ldc, c_is_zero, s);     \
+               : run_tsm2r_pass<T, NTV>(di, ws, impl, m, k, w, A, lda, Bp, ldb, Cp, ldc, c_is_zero, determ, s); \
     break;
     switch (nt) {
       TSM2X_PASS(1)

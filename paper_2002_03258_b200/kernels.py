@@ -100,11 +100,13 @@ def _ld(t, rows: int) -> int:
 
 
 def gemm(A, B, C, *, variant=Variant.V3, params=None, c_is_zero: bool = False, impl: str = "auto",
-         stream=None, check_zero_c: bool = False):
+         stream=None, check_zero_c: bool = False, deterministic: bool = False):
     """In place on device: ``C (+)= A @ B`` for column-major CUDA tensors (fp32 or fp64).
 
-    ``c_is_zero`` elides the read of C (the L_OPT2 contract). Stream-ordered on ``stream``
-    (default: torch's current stream); returns C.
+    ``c_is_zero`` elides the read of C (the L_OPT2 contract). ``deterministic`` selects the
+    static-split kernel whose result is bitwise reproducible run to run (the default dynamic
+    kernel combines split row blocks with fp64 atomics: same tolerance, last-bit variation).
+    Stream-ordered on ``stream`` (default: torch's current stream); returns C.
     """
     import torch
     from .core import KernelParams
@@ -121,7 +123,8 @@ def gemm(A, B, C, *, variant=Variant.V3, params=None, c_is_zero: bool = False, i
         params = KernelParams(t1=128, t2=min(4, n), t3=4, tcf=1, variant=variant)
     validate_params_for(params, m, k, n)
     prec = _lib.DOUBLE if A.dtype == torch.float64 else _lib.SINGLE
-    flags = (_lib.FLAG_C_IS_ZERO if c_is_zero else 0) | (_lib.FLAG_CHECK_ZERO_C if check_zero_c else 0)
+    flags = (_lib.FLAG_C_IS_ZERO if c_is_zero else 0) | (_lib.FLAG_CHECK_ZERO_C if check_zero_c else 0) | \
+        (_lib.FLAG_DETERMINISTIC if deterministic else 0)
     if stream is None:
         stream = torch.cuda.current_stream(A.device)
     p = _params_struct(params)

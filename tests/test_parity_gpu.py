@@ -83,8 +83,10 @@ def test_device_impls_ragged(impl, variant):
             _check(Ct.cpu().numpy(), naive_gemm(A, B, C0), k, prec, what=(impl, variant, m, k, n, prec))
 
 
-def test_aligned_tma_many_shapes():
-    """The TMA path on padded (aligned) layouts, covering k tails, row tails and stream-K splits."""
+@pytest.mark.parametrize("det", [False, True])
+def test_aligned_tma_many_shapes(det):
+    """The TMA path on padded (aligned) layouts, covering k tails, row tails and split row blocks,
+    for the dynamic (default) and the deterministic static-split kernels."""
     import torch
     tsm = _tsm()
     rng = np.random.default_rng(7)
@@ -99,29 +101,33 @@ def test_aligned_tma_many_shapes():
             C = tsm.colmajor_empty(m, n, dt, "cuda")
             C0 = rng.random((m, n))
             C.copy_(torch.from_numpy(C0).to(dt))
-            tsm.gemm(A, B, C, impl="tma")
+            tsm.gemm(A, B, C, impl="tma", deterministic=det)
             torch.cuda.synchronize()
             An, Bn = A.cpu().numpy(), B.cpu().numpy()
             ref = naive_gemm(An, Bn, C0.astype(An.dtype))
             _check(C.cpu().numpy(), ref, k, "double" if dt == torch.float64 else "single", what=(m, k, n, dt))
 
 
-def test_deterministic_repeat():
-    """Fixed-order stream-K combine: two launches give bitwise-identical C."""
+@pytest.mark.parametrize("dt", ["float64", "float32"])
+def test_deterministic_repeat(dt):
+    """deterministic=True (static split, fixed-order combine): launches give bitwise-identical C;
+    the default dynamic kernel agrees with it within tolerance."""
     import torch
     tsm = _tsm()
     m, k, n = 6000, 20000, 8
-    A = tsm.colmajor_empty(m, k, torch.float64, "cuda")
+    dtype = getattr(torch, dt)
+    A = tsm.colmajor_empty(m, k, dtype, "cuda")
     tsm.fill_uniform(A, seed=11)
-    B = tsm.colmajor_empty(k, n, torch.float64, "cuda")
+    B = tsm.colmajor_empty(k, n, dtype, "cuda")
     tsm.fill_uniform(B, seed=12)
     outs = []
-    for _ in range(3):
-        C = tsm.colmajor_empty(m, n, torch.float64, "cuda")
-        C.zero_()
-        tsm.gemm(A, B, C, c_is_zero=True)
+    for det in (True, True, True, False):
+        C = tsm.colmajor_empty(m, n, dtype, "cuda")
+        C.fill_(1.0)
+        tsm.gemm(A, B, C, deterministic=det)
         outs.append(C.cpu().numpy())
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    _check(outs[3], outs[0].astype(np.float64), k, "double" if dt == "float64" else "single")
 
 
 def test_fill_uniform_matches_host_rng():
@@ -266,3 +272,33 @@ def test_config4_fp32_sampled():
         rows = range(r0, r0 + 128)
         ref = naive_gemm(uniform_block(rows, range(k), 31, np.float32), Bh, np.zeros((128, n), np.float32))
         _check(Ch[r0:r0 + 128], ref, k, "single", what=r0)
+
+
+@pytest.mark.parametrize("consumer", ["fma", "dmma", "ffma2"])
+def test_consumer_policies_subprocess(consumer):
+    """Each TMA consumer policy (TSM2X_CONSUMER override) on split and single-chunk shapes."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, sys
+sys.path.insert(0, ".")
+import paper_2002_03258_b200 as tsm
+from oracle import naive_gemm, rel_frobenius
+rng = np.random.default_rng(5)
+for (m, k, n) in [(2000, 5000, 16), (1500, 3001, 8), (777, 10000, 12), (4096, 16, 16), (513, 20000, 3)]:
+    for dt in (torch.float64, torch.float32):
+        A = tsm.colmajor_empty(m, k, dt, "cuda"); A.copy_(torch.from_numpy(rng.random((m, k))).to(dt))
+        B = tsm.colmajor_empty(k, n, dt, "cuda"); B.copy_(torch.from_numpy(rng.random((k, n))).to(dt))
+        C = tsm.colmajor_empty(m, n, dt, "cuda"); C0 = rng.random((m, n)); C.copy_(torch.from_numpy(C0).to(dt))
+        tsm.gemm(A, B, C)
+        ref = naive_gemm(A.cpu().numpy(), B.cpu().numpy(), C0.astype(A.cpu().numpy().dtype))
+        err = rel_frobenius(C.cpu().numpy(), ref)
+        tol = 1e-12 if dt == torch.float64 else 1e-5
+        assert err <= tol, (m, k, n, dt, err)
+print("ok")
+'''
+    env = dict(os.environ, TSM2X_CONSUMER=consumer)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <vector>
 #include <algorithm>
+#include <string>
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
   fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); exit(1);} } while (0)
@@ -193,6 +194,20 @@ static int g_iters;
 int main(int argc, char** argv) {
   cudaDeviceProp prop; CK(cudaGetDeviceProperties(&prop, 0));
   int sms = prop.multiProcessorCount;
+  if (argc > 1 && std::string(argv[1]) == "--sustain") {
+    size_t bytes = (size_t)8 << 30;
+    CK(cudaMalloc(&g_buf, bytes)); CK(cudaMemset(g_buf, 0, bytes)); CK(cudaMalloc(&g_sink, 64));
+    g_n2 = bytes / 16;
+    cudaEvent_t a, b; CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
+    for (int i = 0; i < 1000; ++i) {
+      if (i == 500) CK(cudaEventRecord(a));
+      read_ldg<8><<<sms * 2, 512>>>(g_buf, g_n2, g_sink);
+    }
+    CK(cudaEventRecord(b)); CK(cudaEventSynchronize(b));
+    float ms; CK(cudaEventElapsedTime(&ms, a, b));
+    printf("{\"test\": \"read_ldg_sustained_2nd_half\", \"GBps\": %.1f}\n", 500.0 * bytes / ms / 1e6);
+    return 0;
+  }
   printf("{\"device\": \"%s\", \"sms\": %d, \"l2_bytes\": %d, \"smem_optin\": %zu}\n", prop.name, sms, prop.l2CacheSize, prop.sharedMemPerBlockOptin);
   size_t bytes = (size_t)8 << 30;  // 8 GiB, far above L2
   CK(cudaMalloc(&g_buf, bytes)); CK(cudaMemset(g_buf, 0, bytes)); CK(cudaMalloc(&g_sink, 64));

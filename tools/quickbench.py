@@ -15,12 +15,12 @@ import paper_2002_03258_b200 as tsm  # noqa: E402
 def time_gemm(A, B, C, impl, variant, c_is_zero, reps=10):
     s = torch.cuda.current_stream()
     for _ in range(3):
-        tsm.gemm(A, B, C, impl=impl, variant=variant, c_is_zero=c_is_zero)
+        tsm.gemm(A, B, C, impl=impl.replace("_det", ""), variant=variant, c_is_zero=c_is_zero, deterministic=impl.endswith("_det"))
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
     for i in range(reps):
         ev[2 * i].record(s)
-        tsm.gemm(A, B, C, impl=impl, variant=variant, c_is_zero=c_is_zero)
+        tsm.gemm(A, B, C, impl=impl.replace("_det", ""), variant=variant, c_is_zero=c_is_zero, deterministic=impl.endswith("_det"))
         ev[2 * i + 1].record(s)
     torch.cuda.synchronize()
     ts = sorted(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(reps))
@@ -53,7 +53,7 @@ def main():
         czero = variant == "l-opt2"
         by = eb * (m * k + k * n + (1 if czero else 2) * m * n)
         fl = 2.0 * m * k * n
-        impls = args.impls.split(",") if k > 64 else ["auto"]
+        impls = args.impls.split(",")
         for impl in impls:
             ms = time_gemm(A, B, C, impl, variant, czero)
             print(json.dumps({"cfg": name, "impl": impl, "m": m, "k": k, "n": n, "ms": round(ms, 4),
@@ -63,5 +63,59 @@ def main():
         torch.cuda.empty_cache()
 
 
+
+
+def sustain_main():
+    """Sustained-load probe: each config back to back for ~2 s with NVML clock/power sampling."""
+    import threading
+    import time
+
+    import pynvml
+    pynvml.nvmlInit()
+    h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    cfgs = [("r8", 30720, 30720, 8, torch.float64), ("r2", 30720, 30720, 2, torch.float64),
+            ("r16", 30720, 30720, 16, torch.float64), ("f16", 32768, 32768, 16, torch.float32)]
+    for name, m, k, n, dt in cfgs:
+        A = tsm.colmajor_empty(m, k, dt, "cuda")
+        tsm.fill_uniform(A, 1)
+        B = tsm.colmajor_empty(k, n, dt, "cuda")
+        tsm.fill_uniform(B, 2)
+        C = tsm.colmajor_empty(m, n, dt, "cuda")
+        C.zero_()
+        for det in (False, True):
+            samples = []
+            stop = threading.Event()
+
+            def sampler():
+                while not stop.is_set():
+                    samples.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                    pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0))
+                    time.sleep(0.02)
+            th = threading.Thread(target=sampler)
+            th.start()
+            reps = 1800
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record()
+            for i in range(reps):
+                if i == reps // 2:
+                    ev[1].record()
+                tsm.gemm(A, B, C, deterministic=det)
+            ev[2].record()
+            torch.cuda.synchronize()
+            stop.set()
+            th.join()
+            half = samples[len(samples) // 2:]
+            med = sorted(s[0] for s in half)[len(half) // 2]
+            pw = sorted(s[1] for s in half)[len(half) // 2]
+            ms2 = ev[1].elapsed_time(ev[2]) / (reps - reps // 2)
+            print(json.dumps({"sustain": name, "det": det, "ms_2nd_half": round(ms2, 4), "sm_mhz": med,
+                              "power_w": pw}), flush=True)
+        del A, B, C
+        torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
-    main()
+    if "--sustain" in sys.argv:
+        sustain_main()
+    else:
+        main()
