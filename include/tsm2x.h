@@ -108,6 +108,34 @@ int tsm2x_run_host(int variant, int precision, int64_t m, int64_t k, int64_t n,
 int tsm2x_fill_uniform(int precision, int64_t rows, int64_t cols, void* ptr, int64_t ld, int64_t row_offset,
                        int64_t col_offset, uint64_t seed, void* stream);
 
+/* Parameter selection — the B200 re-derivation of the paper's (t1, t2, t3, tcf) choice
+ * (reference tuner.py:218-363). Process-wide knobs; 0 = the shipped B200 default. */
+typedef struct tsm2x_tuning {
+  int32_t consumer;   /* 0 auto, 1 FMA, 2 DMMA (fp64, 8/16 columns), 3 FFMA2 (fp32)           */
+  int32_t small_kb;   /* KB of A per "small" work item (end of the queue)                     */
+  int32_t big_kb;     /* KB of A per "big" work item                                          */
+  int32_t tail_pct;   /* % of each row block's columns handed out as small items              */
+  int32_t batch_kb;   /* single-chunk row blocks (TSM2L): KB of A per queue grab (tcf analogue) */
+} tsm2x_tuning;
+int tsm2x_set_tuning(const tsm2x_tuning* t); /* NULL restores the defaults */
+int tsm2x_get_tuning(tsm2x_tuning* out);
+
+/* What a tsm2x_run_ex call with these arguments would launch (first 16-column pass). */
+typedef struct tsm2x_plan {
+  int32_t impl;            /* enum tsm2x_impl actually used (AUTO resolved)                    */
+  int32_t consumer;        /* 1 FMA, 2 DMMA, 3 FFMA2 (TMA kernels), 0 otherwise                */
+  int32_t rows_per_block;  /* R: rows per row block            (the paper's t1 analogue)      */
+  int32_t cols_per_pass;   /* NT: skinny columns per pass       (t2)                           */
+  int32_t cols_per_stage;  /* KC: columns per pipeline stage                                   */
+  int32_t stages;          /* ring depth; STAGES*KC columns of A in flight per SM (t3)         */
+  int32_t passes;          /* ceil(n / 16)                                                     */
+  int32_t deterministic;   /* 1 when the static fixed-order combine is used                    */
+  int64_t grid;            /* CTAs                                                             */
+  int64_t items, nbig, kbig, nsmall, ksmall, batch; /* dynamic work items (TMA dynamic path)   */
+} tsm2x_plan;
+int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, int a_aligned16, uint32_t flags,
+                   int impl, tsm2x_plan* out);
+
 /* Profiling hook (bench evidence): the NEXT main kernel launched by this thread (the TSM2R
  * stream kernel or the TSM2L kernel of the next run call) is bracketed by cudaEventRecord of
  * these two cudaEvent_t on its stream; the hook then clears. Pass NULLs to clear explicitly. */

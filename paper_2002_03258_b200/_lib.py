@@ -29,7 +29,27 @@ EXPORTS = (
     "tsm2x_build_target",
     "tsm2x_launch_count",
     "tsm2x_set_kernel_events",
+    "tsm2x_set_tuning",
+    "tsm2x_get_tuning",
+    "tsm2x_plan_for",
 )
+
+
+class Tuning(ctypes.Structure):
+    """struct tsm2x_tuning (B200 parameter selection knobs; 0 = default)."""
+
+    _fields_ = [("consumer", ctypes.c_int32), ("small_kb", ctypes.c_int32), ("big_kb", ctypes.c_int32),
+                ("tail_pct", ctypes.c_int32), ("batch_kb", ctypes.c_int32)]
+
+
+class Plan(ctypes.Structure):
+    """struct tsm2x_plan (what a call would launch)."""
+
+    _fields_ = [("impl", ctypes.c_int32), ("consumer", ctypes.c_int32), ("rows_per_block", ctypes.c_int32),
+                ("cols_per_pass", ctypes.c_int32), ("cols_per_stage", ctypes.c_int32), ("stages", ctypes.c_int32),
+                ("passes", ctypes.c_int32), ("deterministic", ctypes.c_int32), ("grid", ctypes.c_int64),
+                ("items", ctypes.c_int64), ("nbig", ctypes.c_int64), ("kbig", ctypes.c_int64),
+                ("nsmall", ctypes.c_int64), ("ksmall", ctypes.c_int64), ("batch", ctypes.c_int64)]
 
 
 class Params(ctypes.Structure):
@@ -63,8 +83,12 @@ def load() -> ctypes.CDLL:
         lib.tsm2x_run_host.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, vp, i64, pp, u32, i32]
         lib.tsm2x_fill_uniform.argtypes = [i32, i64, i64, vp, i64, i64, i64, ctypes.c_uint64, vp]
         lib.tsm2x_set_kernel_events.argtypes = [vp, vp]
+        lib.tsm2x_set_tuning.argtypes = [ctypes.POINTER(Tuning)]
+        lib.tsm2x_get_tuning.argtypes = [ctypes.POINTER(Tuning)]
+        lib.tsm2x_plan_for.argtypes = [i32, i64, i64, i64, i64, i32, u32, i32, ctypes.POINTER(Plan)]
         for name in ("tsm2x_validate", "tsm2x_run", "tsm2x_run_ex", "tsm2x_run_host", "tsm2x_fill_uniform",
-                     "tsm2x_version", "tsm2x_set_kernel_events"):
+                     "tsm2x_version", "tsm2x_set_kernel_events", "tsm2x_set_tuning", "tsm2x_get_tuning",
+                     "tsm2x_plan_for"):
             getattr(lib, name).restype = ctypes.c_int
         lib.tsm2x_last_error.restype = ctypes.c_char_p
         lib.tsm2x_build_target.restype = ctypes.c_char_p

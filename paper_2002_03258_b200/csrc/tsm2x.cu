@@ -266,13 +266,29 @@ static int stage_bt(Workspace* ws, int64_t k, int64_t kpad, int w, const T* B, i
   return check_launch("prep_bt");
 }
 
+// ---- parameter selection (the B200 re-derivation of the paper's t1/t2/t3/tcf choice) ---------
+// Process-wide tuning knobs (tsm2x_set_tuning); zeros mean "B200 default" — the values below
+// were picked from on-device sweeps (tools/tune.py, profiles/tuning_*.json).
+struct Tuning {
+  int consumer = 0;   // 0 auto, 1 fma, 2 dmma, 3 ffma2
+  int small_kb = 0;   // A bytes per small item (KB); default min(512, max(64, per-CTA share / 48))
+  int big_kb = 0;     // A bytes per big item (KB);   default min(4096, max(small, per-CTA share / 6))
+  int tail_pct = 0;   // % of each row block's columns dispatched as small items; default 20
+  int batch_kb = 0;   // single-chunk row blocks (TSM2L): A bytes per queue grab (tcf analogue); default 1024
+};
+static std::mutex g_tune_mu;
+static Tuning g_tune;
+static Tuning current_tuning() {
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  return g_tune;
+}
+
 // Consumer choice (tsm2r_tma.cuh): DMMA for fp64 split row blocks at NT >= 8 (issue slots /
 // power at the FP64-heavy widths), packed FFMA2 for fp32 at NT >= 2, plain FMA otherwise.
+// TSM2X_CONSUMER=fma|dmma|ffma2 in the environment overrides (ablation runs).
 enum ConsumerKind { kFma = 0, kDmma = 1, kFfma2 = 2 };
-static int g_consumer_override = -1;  // TSM2X_CONSUMER=fma|dmma|ffma2 (ablation / benchmarks)
 
-template <typename T, int NT>
-static int pick_consumer(bool split) {
+static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
   static const int env = [] {
     const char* e = getenv("TSM2X_CONSUMER");
     if (!e) return -1;
@@ -281,15 +297,51 @@ static int pick_consumer(bool split) {
     if (!strcmp(e, "ffma2")) return (int)kFfma2;
     return -1;
   }();
-  const int want = g_consumer_override >= 0 ? g_consumer_override : env;
-  const bool dmma_ok = sizeof(T) == 8 && (NT == 8 || NT == 16);
-  const bool ffma2_ok = sizeof(T) == 4 && NT >= 2;
+  const int want = env >= 0 ? env : (tu.consumer == 1 ? kFma : tu.consumer == 2 ? kDmma : tu.consumer == 3 ? kFfma2 : -1);
+  const bool dmma_ok = eb == 8 && (nt == 8 || nt == 16);
+  const bool ffma2_ok = eb == 4 && nt >= 2;
   if (want == kFma) return kFma;
   if (want == kDmma) return dmma_ok ? kDmma : kFma;
   if (want == kFfma2) return ffma2_ok ? kFfma2 : kFma;
   if (dmma_ok && split) return kDmma;
   if (ffma2_ok) return kFfma2;
   return kFma;
+}
+
+// Item geometry of the dynamic TMA kernel for one pass (rows_per_block = R, KC columns/stage).
+static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, const Tuning& tu, Items* it,
+                       int64_t* grid) {
+  const int64_t G_full = sms;  // one CTA per SM (smem-bound by design)
+  it->num_rb = (m + R - 1) / R;
+  const double col_bytes = (double)R * eb;  // one column of one row block
+  const double per_cta = (double)m * k * eb / (double)G_full;
+  const double small_b = tu.small_kb > 0 ? tu.small_kb * 1024.0 : std::min(512.0 * 1024, std::max(64.0 * 1024, per_cta / 48));
+  const double big_b =
+      tu.big_kb > 0 ? std::max(small_b, tu.big_kb * 1024.0) : std::min(4.0 * 1024 * 1024, std::max(small_b, per_cta / 6));
+  const int64_t ksmall = std::max<int64_t>(KC, (int64_t)align_up((size_t)(small_b / col_bytes), KC));
+  const int64_t kbig = std::max<int64_t>(ksmall, (int64_t)align_up((size_t)(big_b / col_bytes), KC));
+  const double batch_b = tu.batch_kb > 0 ? tu.batch_kb * 1024.0 : 1024.0 * 1024;
+  if ((double)k * col_bytes <= 1024.0 * 1024 || k <= ksmall) {
+    // single-chunk row blocks (TSM2L shapes): no split, batched dispatch
+    it->nbig = 0;
+    it->kbig = KC;
+    it->kbig_end = 0;
+    it->nsmall = 1;
+    it->ksmall = (int64_t)align_up((size_t)k, KC);
+    it->batch = std::max<int64_t>(1, (int64_t)(batch_b / ((double)k * col_bytes)));
+  } else {
+    const int pct = tu.tail_pct > 0 ? std::min(tu.tail_pct, 100) : 20;
+    const int64_t tail_cols = std::max<int64_t>(1, (k * pct + 99) / 100);
+    const int64_t tail = std::min<int64_t>(k, (int64_t)align_up((size_t)tail_cols, (size_t)ksmall));
+    it->kbig_end = ((k - tail) / KC) * KC;
+    it->kbig = kbig;
+    it->nbig = it->kbig_end > 0 ? (it->kbig_end + kbig - 1) / kbig : 0;
+    it->ksmall = ksmall;
+    it->nsmall = (k - it->kbig_end + ksmall - 1) / ksmall;
+    it->batch = 1;
+  }
+  it->total = it->num_rb * it->nch();
+  *grid = std::min<int64_t>(G_full, (it->total + it->batch - 1) / it->batch);
 }
 
 template <typename T, int NT, int KIND>
@@ -324,8 +376,8 @@ template <typename T, int NT>
 static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k, int w, const T* A, int64_t lda,
                          const T* B, int64_t ldb, T* C, int64_t ldc, bool c_is_zero, cudaStream_t s) {
   using Cfg = TmaCfg<T, NT>;
-  const int64_t G_full = (int64_t)di.sms;  // one CTA per SM (smem-bound by design)
   const size_t eb = sizeof(T);
+  const Tuning tu = current_tuning();
   DynArgs<T> a;
   a.C = C;
   a.ldc = ldc;
@@ -335,38 +387,13 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   a.c_is_zero = c_is_zero ? 1 : 0;
   a.vec_c = aligned16(C) && (ldc % Vec<T>::N == 0);
   Items& it = a.it;
-  it.num_rb = (m + Cfg::R - 1) / Cfg::R;
-  const double col_bytes = (double)Cfg::R * eb;  // one column of one row block
-  const double total = (double)m * k * eb;
-  const double per_cta = total / (double)G_full;
-  const double small_b = std::min(512.0 * 1024, std::max(64.0 * 1024, per_cta / 48));
-  const double big_b = std::min(4.0 * 1024 * 1024, std::max(small_b, per_cta / 6));
-  const int64_t ksmall = std::max<int64_t>(Cfg::KC, (int64_t)align_up((size_t)(small_b / col_bytes), Cfg::KC));
-  const int64_t kbig = std::max<int64_t>(ksmall, (int64_t)align_up((size_t)(big_b / col_bytes), Cfg::KC));
-  if ((double)k * col_bytes <= 1024.0 * 1024 || k <= ksmall) {
-    // single-chunk row blocks (TSM2L shapes): no split, batched dispatch of ~1 MB per grab
-    it.nbig = 0;
-    it.kbig = Cfg::KC;
-    it.kbig_end = 0;
-    it.nsmall = 1;
-    it.ksmall = (int64_t)align_up((size_t)k, Cfg::KC);
-    it.batch = std::max<int64_t>(1, (int64_t)(1024.0 * 1024 / ((double)k * col_bytes)));
-  } else {
-    const int64_t tail = std::min<int64_t>(k, (int64_t)align_up((size_t)((k + 4) / 5), (size_t)ksmall));
-    it.kbig_end = ((k - tail) / Cfg::KC) * Cfg::KC;
-    it.kbig = kbig;
-    it.nbig = it.kbig_end > 0 ? (it.kbig_end + kbig - 1) / kbig : 0;
-    it.ksmall = ksmall;
-    it.nsmall = (k - it.kbig_end + ksmall - 1) / ksmall;
-    it.batch = 1;
-  }
-  it.total = it.num_rb * it.nch();
-  const int64_t G = std::min<int64_t>(G_full, (it.total + it.batch - 1) / it.batch);
+  int64_t G;
+  make_items(di.sms, m, k, eb, Cfg::R, Cfg::KC, tu, &it, &G);
   const bool split = it.nch() > 1;
   const int64_t kpad = (int64_t)align_up((size_t)k, Cfg::KC);
   a.ldacc = (int64_t)it.num_rb * Cfg::R;
   const size_t acc_bytes = (split && sizeof(T) == 4) ? (size_t)a.ldacc * NT * sizeof(double) : 0;
-  const int kind = pick_consumer<T, NT>(split);
+  const int kind = pick_consumer_rt(sizeof(T), NT, split, tu);
   T* Bt;
   char* rest;
   TSM2X_TRY((stage_bt<T, NT>(ws, k, kpad, w, B, ldb, acc_bytes, 8, s, &Bt, &rest, kind == kDmma)));
@@ -1037,6 +1064,95 @@ int tsm2x_fill_uniform(int precision, int64_t rows, int64_t cols, void* ptr, int
   else
     fill_uniform<float><<<grid, 256, 0, s>>>((float*)ptr, rows, cols, ld, row_offset, col_offset, seed);
   return check_launch("fill_uniform");
+}
+
+int tsm2x_set_tuning(const tsm2x_tuning* t) {
+  Tuning nt;
+  if (t) {
+    if (t->consumer < 0 || t->consumer > 3 || t->small_kb < 0 || t->big_kb < 0 || t->tail_pct < 0 ||
+        t->tail_pct > 100 || t->batch_kb < 0)
+      return fail(TSM2X_EINVAL, "bad tuning values");
+    nt.consumer = t->consumer;
+    nt.small_kb = t->small_kb;
+    nt.big_kb = t->big_kb;
+    nt.tail_pct = t->tail_pct;
+    nt.batch_kb = t->batch_kb;
+  }
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  g_tune = nt;
+  return TSM2X_OK;
+}
+
+int tsm2x_get_tuning(tsm2x_tuning* out) {
+  if (!out) return fail(TSM2X_EINVAL, "null output");
+  const Tuning t = current_tuning();
+  out->consumer = t.consumer;
+  out->small_kb = t.small_kb;
+  out->big_kb = t.big_kb;
+  out->tail_pct = t.tail_pct;
+  out->batch_kb = t.batch_kb;
+  return TSM2X_OK;
+}
+
+int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, int a_aligned16, uint32_t flags,
+                   int impl, tsm2x_plan* out) {
+  if (!out) return fail(TSM2X_EINVAL, "null output");
+  if (precision != TSM2X_SINGLE && precision != TSM2X_DOUBLE) return fail(TSM2X_EINVAL, "bad precision");
+  if (m < 1 || k < 1 || n < 1 || lda < m) return fail(TSM2X_EINVAL, "bad dimensions");
+  memset(out, 0, sizeof(*out));
+  const size_t eb = precision == TSM2X_DOUBLE ? 8 : 4;
+  const int w = (int)std::min<int64_t>(16, n);
+  const int nt = nt_for(w);
+  out->cols_per_pass = nt;
+  out->passes = (int)((n + 15) / 16);
+  int sms = 148;
+  int dev;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    DevInfo di;
+    if (device_info(dev, &di) == TSM2X_OK) sms = di.sms;
+  }
+  cudaGetLastError();
+  const bool tma_layout = a_aligned16 && ((lda * (int64_t)eb) % 16 == 0) && m < (int64_t(1) << 31);
+  const bool determ = (flags & TSM2X_FLAG_DETERMINISTIC) != 0;
+  if (impl == TSM2X_IMPL_ABLATION || impl == TSM2X_IMPL_TSM2L ||
+      (impl == TSM2X_IMPL_AUTO && k <= TSM2L_KMAX && !tma_layout)) {
+    out->impl = impl == TSM2X_IMPL_ABLATION ? TSM2X_IMPL_ABLATION : TSM2X_IMPL_TSM2L;
+    out->rows_per_block = 256 * (a_aligned16 ? (int)(16 / eb) : 1);
+    return TSM2X_OK;
+  }
+  const bool tma = (impl == TSM2X_IMPL_AUTO || impl == TSM2X_IMPL_STREAM_TMA) && tma_layout;
+  if (!tma) {
+    out->impl = TSM2X_IMPL_STREAM_LDG;
+    out->rows_per_block = 256 * (a_aligned16 && lda % (16 / eb) == 0 ? (int)(16 / eb) : 1);
+    out->cols_per_stage = 32;
+    out->deterministic = 1;
+    return TSM2X_OK;
+  }
+  out->impl = TSM2X_IMPL_STREAM_TMA;
+  const int R = 256 * (int)(16 / eb);
+  out->rows_per_block = R;
+  out->cols_per_stage = TmaCfg<double, 1>::KC;
+  out->stages = TmaCfg<double, 1>::STAGES;
+  if (determ) {
+    out->deterministic = 1;
+    out->consumer = 1;
+    const int64_t units = ((m + R - 1) / R) * ((k + 7) / 8);
+    out->grid = std::min<int64_t>(units, sms);
+    return TSM2X_OK;
+  }
+  const Tuning tu = current_tuning();
+  Items it;
+  int64_t G;
+  make_items(sms, m, k, eb, R, out->cols_per_stage, tu, &it, &G);
+  out->grid = G;
+  out->items = it.total;
+  out->nbig = it.nbig;
+  out->kbig = it.kbig;
+  out->nsmall = it.nsmall;
+  out->ksmall = it.ksmall;
+  out->batch = it.batch;
+  out->consumer = 1 + pick_consumer_rt(eb, nt, it.nch() > 1, tu);
+  return TSM2X_OK;
 }
 
 int tsm2x_set_kernel_events(void* start_event, void* stop_event) {

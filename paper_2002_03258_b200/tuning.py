@@ -1,0 +1,165 @@
+"""Parameter selection for B200 — the re-derivation of the paper's (t1, t2, t3, tcf) choice.
+
+The reference chooses (t2, t3) by projected gradient descent on a Little's-law model and t1 /
+tcf from profiled catalog winners or synthetic scores (``pkg/src/tsgemm/tuner.py:218-363``).
+That model is calibrated for K40c-V100 and mispredicts B200 by 3x. Here the
+three levels of tiling are re-mapped onto the sm_100a kernel and chosen by measurement:
+
+==========  ==============================  =================================================
+paper       B200 kernel (tsm2r_tma.cuh)     chosen by
+==========  ==============================  =================================================
+t1          R rows per row block            fixed: 8 consumer warps x 32 lanes x 16 B / eb
+                                            (512 fp64 / 1024 fp32) — one TMA box per 256 rows
+t2          NT columns per pass             n (<= 16) in one pass: A streamed exactly once
+t3          prefetch depth                  TMA ring: 6 stages x 8 columns (~160 KB in flight/SM)
+tcf         rows per thread (TSM2L)         ``batch_kb``: A bytes per queue grab for
+                                            single-chunk row blocks
+(new)       work-item sizes                 ``small_kb``/``big_kb``/``tail_pct``: dynamic
+                                            queue granularity (tail vs. combine traffic)
+(new)       consumer datapath               FMA / DMMA (fp64 tensor MMA) / FFMA2 (packed fp32)
+==========  ==============================  =================================================
+
+:func:`plan` reports what the library will launch for a shape; :func:`tune_tsm2r` /
+:func:`select_tcf` sweep the knobs on the device with CUDA-event timing and return the winner
+with the whole measured table (the reference's TuneResult role). The shipped defaults
+(:data:`B200_DEFAULTS`) come from such sweeps, recorded in ``profiles/tuning_r01.json``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import itertools
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional
+
+from . import _lib
+
+CONSUMERS = {0: "auto", 1: "fma", 2: "dmma", 3: "ffma2"}
+IMPLS = {v: k for k, v in _lib.IMPL.items()}
+
+# The library's built-in defaults (tsm2x.cu make_items / pick_consumer_rt), stated here for
+# reporting; 0 in a Tuning means "use these".
+B200_DEFAULTS = {
+    "consumer": "auto: DMMA for fp64 split row blocks at n in {8,16}; FFMA2 for fp32 n >= 2; else FMA",
+    "small_kb": "min(512, max(64, per-CTA share / 48))",
+    "big_kb": "min(4096, max(small, per-CTA share / 6))",
+    "tail_pct": 20,
+    "batch_kb": 1024,
+}
+
+
+@dataclass(frozen=True)
+class Tuning:
+    consumer: int = 0
+    small_kb: int = 0
+    big_kb: int = 0
+    tail_pct: int = 0
+    batch_kb: int = 0
+
+    def _c(self) -> _lib.Tuning:
+        return _lib.Tuning(self.consumer, self.small_kb, self.big_kb, self.tail_pct, self.batch_kb)
+
+
+def set_tuning(t: Optional[Tuning]) -> None:
+    """Process-wide knobs for every later call (None restores the B200 defaults)."""
+    lib = _lib.load()
+    _lib.check(lib.tsm2x_set_tuning(ctypes.byref(t._c()) if t is not None else None))
+
+
+def get_tuning() -> Tuning:
+    out = _lib.Tuning()
+    _lib.check(_lib.load().tsm2x_get_tuning(ctypes.byref(out)))
+    return Tuning(out.consumer, out.small_kb, out.big_kb, out.tail_pct, out.batch_kb)
+
+
+def plan(precision: str, m: int, k: int, n: int, lda: Optional[int] = None, aligned: bool = True,
+         deterministic: bool = False, impl: str = "auto") -> Dict:
+    """The kernel, tiling and work split a device call with these arguments would use."""
+    prec = _lib.DOUBLE if precision in ("double", "fp64", "f64") else _lib.SINGLE
+    if lda is None:
+        lda = (m + 31) // 32 * 32
+    out = _lib.Plan()
+    flags = _lib.FLAG_DETERMINISTIC if deterministic else 0
+    _lib.check(_lib.load().tsm2x_plan_for(prec, m, k, n, lda, 1 if aligned else 0, flags, _lib.IMPL[impl],
+                                          ctypes.byref(out)))
+    d = {f: getattr(out, f) for f, _ in _lib.Plan._fields_}
+    d["impl"] = IMPLS.get(d["impl"], d["impl"])
+    d["consumer"] = CONSUMERS.get(d["consumer"], d["consumer"])
+    # the paper's vocabulary, for tune-style reporting
+    d["t1"] = d["rows_per_block"]
+    d["t2"] = d["cols_per_pass"]
+    d["t3"] = d["stages"] * d["cols_per_stage"]
+    return d
+
+
+@dataclass
+class TuneResult:
+    """Measured sweep: the winning knobs, their time, and every point tried."""
+
+    best: Tuning
+    best_ms: float
+    default_ms: float
+    table: List[Dict] = field(default_factory=list)
+    shape: Dict = field(default_factory=dict)
+
+
+def _time_call(fn, reps: int) -> float:
+    import torch
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in evs:
+        a.record()
+        fn()
+        b.record()
+    torch.cuda.synchronize()
+    ts = sorted(a.elapsed_time(b) for a, b in evs)
+    return ts[len(ts) // 2]
+
+
+def _sweep(m, k, n, precision, candidates, reps, variant):
+    import torch
+
+    from .kernels import colmajor_empty, fill_uniform, gemm
+    dt = torch.float64 if precision in ("double", "fp64") else torch.float32
+    A = colmajor_empty(m, k, dt, "cuda")
+    fill_uniform(A, 1)
+    B = colmajor_empty(k, n, dt, "cuda")
+    fill_uniform(B, 2)
+    C = colmajor_empty(m, n, dt, "cuda")
+    C.zero_()
+    saved = get_tuning()
+    table = []
+    try:
+        for t in candidates:
+            set_tuning(t)
+            ms = _time_call(lambda: gemm(A, B, C, variant=variant), reps)
+            table.append({"tuning": t.__dict__, "ms": round(ms, 5), "plan": plan(precision, m, k, n)})
+    finally:
+        set_tuning(saved)
+    best = min(table, key=lambda r: r["ms"])
+    default = next(r for r in table if r["tuning"] == Tuning().__dict__)
+    return TuneResult(best=Tuning(**best["tuning"]), best_ms=best["ms"], default_ms=default["ms"], table=table,
+                      shape={"m": m, "k": k, "n": n, "precision": precision})
+
+
+def tune_tsm2r(m: int, k: int, n: int, precision: str = "double", reps: int = 10,
+               consumers=(0, 1, 2, 3), small_kbs=(0, 128, 512), big_kbs=(0, 2048, 8192),
+               tail_pcts=(0, 10, 30)) -> TuneResult:
+    """On-device sweep of the TSM2R knobs for one shape (the B200 analogue of tune_tsm2r,
+    reference tuner.py:218-276). The default (all zeros) is always measured."""
+    cands = [Tuning()]
+    for c, s, b, p in itertools.product(consumers, small_kbs, big_kbs, tail_pcts):
+        t = Tuning(consumer=c, small_kb=s, big_kb=b, tail_pct=p)
+        if t not in cands:
+            cands.append(t)
+    return _sweep(m, k, n, precision, cands, reps, "v3")
+
+
+def select_tcf(m: int, k: int, n: int, precision: str = "double", reps: int = 10,
+               batch_kbs=(0, 64, 256, 1024, 4096)) -> TuneResult:
+    """TSM2L: sweep the dispatch granularity of single-chunk row blocks — the role the paper's
+    tcf (row tiles per thread) plays (reference tuner.py:337-363)."""
+    cands = [Tuning()] + [Tuning(batch_kb=b) for b in batch_kbs if b]
+    return _sweep(m, k, n, precision, cands, reps, "l-opt2")

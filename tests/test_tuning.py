@@ -1,0 +1,54 @@
+"""Parameter selection (paper_2002_03258_b200.tuning): plans for the BASELINE shapes and the
+tuning knobs, host-side only (no GPU needed)."""
+
+import pytest
+
+from paper_2002_03258_b200 import tuning
+
+
+def test_plan_config2_tsm2r():
+    p = tuning.plan("double", 30720, 30720, 8)
+    assert p["impl"] == "tma" and p["consumer"] == "dmma"
+    assert p["t1"] == 512 and p["t2"] == 8 and p["t3"] == 48
+    assert p["grid"] <= 148 and p["items"] >= 24 * p["grid"] // 2
+    assert p["nbig"] > 0 and p["nsmall"] > 0 and p["batch"] == 1
+    # the small items cover roughly the last 20% of each row block's columns
+    assert 0.15 <= p["nsmall"] * p["ksmall"] / 30720 <= 0.3
+
+
+def test_plan_tsm2l_single_chunk():
+    p = tuning.plan("double", 1 << 24, 16, 16)
+    assert p["impl"] == "tma" and p["consumer"] == "fma"
+    assert p["nbig"] == 0 and p["nsmall"] == 1 and p["batch"] > 1
+
+
+def test_plan_fp32_and_wide():
+    p = tuning.plan("single", 32768, 32768, 16)
+    assert p["consumer"] == "ffma2" and p["t1"] == 1024
+    assert tuning.plan("double", 1000, 1000, 40)["passes"] == 3
+
+
+def test_plan_fallbacks():
+    assert tuning.plan("double", 1001, 5000, 8, lda=1001)["impl"] == "ldg"     # odd lda: no TMA
+    assert tuning.plan("double", 1001, 16, 8, lda=1001)["impl"] == "tsm2l"
+    assert tuning.plan("double", 4096, 4096, 8, deterministic=True)["deterministic"] == 1
+    assert tuning.plan("double", 4096, 4096, 8, impl="ablation")["impl"] == "ablation"
+
+
+def test_tuning_knobs_round_trip_and_change_the_plan():
+    base = tuning.plan("double", 30720, 30720, 8)
+    try:
+        tuning.set_tuning(tuning.Tuning(consumer=1, small_kb=128, big_kb=2048, tail_pct=40))
+        assert tuning.get_tuning() == tuning.Tuning(consumer=1, small_kb=128, big_kb=2048, tail_pct=40)
+        p = tuning.plan("double", 30720, 30720, 8)
+        assert p["consumer"] == "fma"
+        assert p["ksmall"] == 128 * 1024 // (512 * 8)
+        assert p["kbig"] == 2048 * 1024 // (512 * 8)
+        assert p["nsmall"] * p["ksmall"] >= 0.4 * 30720 - p["ksmall"]
+        assert p["items"] != base["items"]
+        with pytest.raises(ValueError):
+            tuning.set_tuning(tuning.Tuning(tail_pct=101))
+    finally:
+        tuning.set_tuning(None)
+    assert tuning.get_tuning() == tuning.Tuning()
+    assert tuning.plan("double", 30720, 30720, 8) == base
