@@ -227,10 +227,18 @@ def run_ours(args, wl):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun")
+    # TSM2X_BENCH_SHARE_GPU=1 (test only): all ranks on cuda:0 over gloo, to exercise the
+    # multi-rank path on a one-GPU box; numbers from such a run are not bench values.
+    share = os.environ.get("TSM2X_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     dt = torch.float64 if prec == "double" else torch.float32
     eb = 8 if prec == "double" else 4
     lib = _lib.load()
@@ -321,7 +329,7 @@ def run_ours(args, wl):
             "GBps": round(gbps, 1),
             "roofline": {"bound": "hbm", "achieved": round(kern_gbps, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(kern_gbps / peak, 4), "traffic": traffic,
-                         "kernel": "tsm2r_stream_tma" if k > 64 else "tsm2l_kernel",
+                         "kernel": "tsm2r_stream_tma (dynamic items; single-chunk row blocks when k is small)",
                          "kernel_ms": round(kern_ms, 5), "algorithmic_bytes_per_launch": byts,
                          "peak_source": peak_src,
                          "read_stream_ceiling_gbs": 7300.0,

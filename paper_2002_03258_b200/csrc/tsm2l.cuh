@@ -78,35 +78,50 @@ __global__ void __launch_bounds__(THREADS) tsm2l_kernel(const LArgs<T> a) {
       }
     }
 
-    // epilogue: C columns are contiguous over rows -> one 128-bit access per column when the
-    // whole vector is in range.
+    // epilogue: all reads of C first (one round trip), then the stores; whole vectors in range
+    // use one 128-bit access per column.
+    T old[RPT][NT];
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      if (j < a.w) {
-        T* cj = a.C + (int64_t)j * a.ldc;
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) old[r][j] = T(0);
+    const bool full_vec = VEC && (row0 + RPT <= a.m);
+    if (!a.c_is_zero) {
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        if (j >= a.w) continue;
+        const T* cj = a.C + (int64_t)j * a.ldc;
         if constexpr (VEC) {
-          using V = typename Vec<T>::type;
-          if (row0 + RPT <= a.m) {
-            V* cp = reinterpret_cast<V*>(cj + row0);
-            T out[RPT];
-            if (a.c_is_zero) {
+          if (full_vec) {
+            using V = typename Vec<T>::type;
+            const V v = __ldcs(reinterpret_cast<const V*>(cj + row0));
 #pragma unroll
-              for (int r = 0; r < RPT; ++r) out[r] = acc[r][j];
-            } else {
-              V old = __ldcs(cp);
-#pragma unroll
-              for (int r = 0; r < RPT; ++r) out[r] = vget<T>(old, r) + acc[r][j];
-            }
-            __stcs(cp, vmake<T>(out));
+            for (int r = 0; r < RPT; ++r) old[r][j] = vget<T>(v, r);
             continue;
           }
         }
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          int64_t row = row0 + r;
-          if (row < a.m) cj[row] = a.c_is_zero ? acc[r][j] : cj[row] + acc[r][j];
+        for (int r = 0; r < RPT; ++r)
+          if (row0 + r < a.m) old[r][j] = cj[row0 + r];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      if (j >= a.w) continue;
+      T* cj = a.C + (int64_t)j * a.ldc;
+      T out[RPT];
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) out[r] = old[r][j] + acc[r][j];
+      if constexpr (VEC) {
+        if (full_vec) {
+          using V = typename Vec<T>::type;
+          __stcs(reinterpret_cast<V*>(cj + row0), vmake<T>(out));
+          continue;
         }
       }
+#pragma unroll
+      for (int r = 0; r < RPT; ++r)
+        if (row0 + r < a.m) cj[row0 + r] = out[r];
     }
   }
 }

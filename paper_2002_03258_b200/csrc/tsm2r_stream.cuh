@@ -52,14 +52,22 @@ __device__ __forceinline__ void load_brow(const T* __restrict__ p, T (&b)[NT]) {
 // Epilogue helpers shared by the LDG and TMA stream kernels. acc[r][j] holds rows row0+r.
 template <typename T, int NT, int RPT>
 __device__ __forceinline__ void store_c(const StreamArgs<T>& a, int64_t row0, const T (&acc)[RPT][NT]) {
+  T old[RPT][NT];  // all reads of C first: one round trip instead of NT*RPT dependent ones
+#pragma unroll
+  for (int j = 0; j < NT; ++j)
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int64_t row = row0 + r;
+      old[r][j] = (!a.c_is_zero && j < a.w && row < a.m) ? a.C[j * a.ldc + row] : T(0);
+    }
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
     if (j < a.w) {
       T* cj = a.C + j * a.ldc;
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
-        int64_t row = row0 + r;
-        if (row < a.m) cj[row] = a.c_is_zero ? acc[r][j] : cj[row] + acc[r][j];
+        const int64_t row = row0 + r;
+        if (row < a.m) cj[row] = old[r][j] + acc[r][j];
       }
     }
   }

@@ -116,6 +116,15 @@ template <typename T, int NT, int RPT, int R>
 __device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int ct, const T (&acc)[RPT][NT]) {
   const int64_t row_base = rb * R + ct;
   if (a.it.nch() == 1) {
+    // all loads of C first (one round trip, not NT*RPT dependent ones), then the stores
+    T old[RPT][NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int64_t row = row_base + r * TmaCfg<T, NT>::BOX;
+        old[r][j] = (!a.c_is_zero && j < a.w && row < a.m) ? __ldcs(a.C + j * a.ldc + row) : T(0);
+      }
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       if (j >= a.w) continue;
@@ -123,12 +132,7 @@ __device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
         const int64_t row = row_base + r * TmaCfg<T, NT>::BOX;
-        if (row < a.m) {
-          if (a.c_is_zero)
-            __stcs(cj + row, acc[r][j]);
-          else
-            __stcs(cj + row, __ldcs(cj + row) + acc[r][j]);
-        }
+        if (row < a.m) __stcs(cj + row, old[r][j] + acc[r][j]);
       }
     }
     return;
@@ -308,6 +312,20 @@ struct DmmaConsumer {
     const int g = lane >> 2, t = lane & 3;
     const int64_t base = rb * Cfg::R + 64 * warp + 2 * g;
     const bool split = a.it.nch() > 1;
+    double old[4][2][NTI][2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int64_t row = base + 16 * q + mt;
+            const int j = 8 * nt + 2 * t + e;
+            old[q][mt][nt][e] =
+                (!split && !a.c_is_zero && row < a.m && j < a.w) ? a.C[j * a.ldc + row] : 0.0;
+          }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -324,7 +342,7 @@ struct DmmaConsumer {
             if (split)
               red_add(c, acc[q][mt][nt][e]);
             else
-              *c = a.c_is_zero ? acc[q][mt][nt][e] : *c + acc[q][mt][nt][e];
+              *c = old[q][mt][nt][e] + acc[q][mt][nt][e];
           }
       }
   }

@@ -44,8 +44,19 @@ def broadcast_b(B, k: int, n: int, dtype, device, src: int = 0, group=None):
     buf = colmajor_buffer(k, n, dtype, device)
     if rank == src:
         buf.copy_(B)
-    dist.broadcast(buf.t(), src=src, group=group)  # .t() is the contiguous (n, k) storage
+    if _host_staged(buf, group):
+        host = buf.t().cpu()
+        dist.broadcast(host, src=src, group=group)
+        buf.t().copy_(host)
+    else:
+        dist.broadcast(buf.t(), src=src, group=group)  # .t() is the contiguous (n, k) storage
     return buf
+
+
+def _host_staged(t, group) -> bool:
+    """gloo moves CUDA tensors only for some collectives: stage through host memory there."""
+    import torch.distributed as dist
+    return t.is_cuda and dist.get_backend(group) == "gloo"
 
 
 def run_sharded(A_local, B, C_local, *, k: int, n: int, variant="v3", c_is_zero: bool = False, src: int = 0,
@@ -71,7 +82,9 @@ def gather_c(C_local, m: int, n: int, dst: int = 0, group=None):
     rank = dist.get_rank(group) if group is not None else dist.get_rank()
     shard_rows = [row_partition(m, world, r) for r in range(world)]
     maxr = max(r1 - r0 for r0, r1 in shard_rows)
-    pad = torch.zeros((n, maxr), dtype=C_local.dtype, device=C_local.device)
+    staged = _host_staged(C_local, group)
+    dev = "cpu" if staged else C_local.device
+    pad = torch.zeros((n, maxr), dtype=C_local.dtype, device=dev)
     r0, r1 = shard_rows[rank]
     pad[:, : r1 - r0] = C_local.t()
     gathered = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
