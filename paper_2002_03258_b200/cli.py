@@ -1,0 +1,285 @@
+"""GPU-backed experiment front-end, mirroring the reference CLI's
+subcommands and CSV conventions (reference ``pkg/src/tsgemm/cli.py``: ``run`` 163-187,
+``tune`` 197-214, ``model`` 234-253, ``sweep-tcf`` 265-297; atomic UTF-8/LF CSV with ``repr``
+floats 67-89) — but every number here is MEASURED on the B200 (CUDA events) instead of simulated.
+
+    python -m paper_2002_03258_b200.cli run --m 30720 --k 30720 --n 8 --variant v3 --out run.csv
+    python -m paper_2002_03258_b200.cli tune --m 30720 --k 30720 --n 16 --out tune.csv
+    python -m paper_2002_03258_b200.cli model --out model.csv
+    python -m paper_2002_03258_b200.cli sweep-tcf --k 16 --n 16 --out sweep.csv
+
+``run`` inputs follow the reference's convention (``default_rng([seed, shape_index])``, A then B
+uniform [0,1), C0 = 0; cli.py:132-134) for shapes up to 2^26 elements of A, and the counter-based
+device generator above that. The correctness column is checked against cuBLAS DGEMM on the same
+device (fp64), not against the CPU oracle (the package does not depend on it).
+"""
+
+from __future__ import annotations
+
+import argparse
+import csv
+import json
+import os
+import sys
+import tempfile
+from typing import Iterable, List, Optional, Sequence
+
+import numpy as np
+
+from .core import KernelParams, Precision, Variant, validate_problem
+from . import tuning
+
+# B200 "catalog entry" (the reference keeps per-GPU YAML, data/gpus/*.yaml): measured on this
+# pool's parts by tools/microbench.cu (profiles/README.md) except where noted.
+B200_SPEC = {
+    "name": "B200",
+    "num_sms": 148,
+    "core_clock_max_mhz": 1965,
+    "mem_bandwidth_read_gbs": 7300.0,      # read-only stream
+    "mem_bandwidth_copy_gbs": 6550.0,      # MEASURED_PEAKS.json (driver)
+    "peak_gflops_double": 36400.0,         # DFMA; DMMA m8n8k4 37100 on the same datapath
+    "peak_gflops_single": 71100.0,         # FFMA; FFMA2 73000
+    "shared_per_sm": 233472,
+    "l2_bytes": 132644864,
+    "h2d_gbs": 55.6,
+}
+
+
+def _fmt(v) -> str:
+    if isinstance(v, float):
+        return repr(v)
+    if v is None:
+        return ""
+    return str(v)
+
+
+def _write_csv(path: str, header: Sequence[str], rows: Iterable[Sequence]) -> None:
+    """Atomic: the file appears complete or not at all (reference cli.py:75-89)."""
+    directory = os.path.dirname(os.path.abspath(path)) or "."
+    fd, tmp = tempfile.mkstemp(dir=directory, suffix=".tmp")
+    try:
+        with os.fdopen(fd, "w", encoding="utf-8", newline="") as fh:
+            w = csv.writer(fh, lineterminator="\n")
+            w.writerow(header)
+            for r in rows:
+                w.writerow([_fmt(x) for x in r])
+        os.replace(tmp, path)
+    except BaseException:
+        if os.path.exists(tmp):
+            os.unlink(tmp)
+        raise
+
+
+def _hbm_peak() -> float:
+    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    try:
+        with open(os.path.join(here, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except Exception:
+        return B200_SPEC["mem_bandwidth_copy_gbs"]
+
+
+def _time_ms(fn, reps: int) -> float:
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return sorted(ts)[len(ts) // 2]
+
+
+RUN_HEADER = ["gpu", "precision", "m", "k", "n", "variant", "t1", "t2", "t3", "tcf", "shape_class", "impl",
+              "consumer", "rows_per_block", "cols_per_pass", "cols_per_stage", "stages", "items", "grid",
+              "time_ms", "gflops", "gbps", "hbm_frac", "check_max_rel_err", "check_rel_frobenius", "error"]
+
+
+def _run_point(prec: Precision, shape, variant: Variant, override: dict, seed: int, si: int, reps: int):
+    import torch
+
+    from .kernels import colmajor_empty, fill_uniform, gemm
+    m, k, n = shape
+    base = ["B200", prec.value, m, k, n, variant.value]
+    try:
+        t1 = override.get("t1", 128)
+        t2 = override.get("t2", n)
+        t3 = override.get("t3", min(4, t1))
+        tcf = override.get("tcf", 1) if variant.is_tsm2l else 1
+        params = KernelParams(t1=t1, t2=t2, t3=t3, tcf=tcf, variant=variant)
+        params.validate_for(m, k, n)
+        dt = torch.float64 if prec is Precision.DOUBLE else torch.float32
+        A = colmajor_empty(m, k, dt, "cuda")
+        B = colmajor_empty(k, n, dt, "cuda")
+        if m * k <= (1 << 26):
+            rng = np.random.default_rng([seed, si])
+            a = rng.random(m * k, dtype=np.float64).astype(prec.dtype).reshape((m, k), order="F")
+            b = rng.random(k * n, dtype=np.float64).astype(prec.dtype).reshape((k, n), order="F")
+            A.copy_(torch.from_numpy(a))
+            B.copy_(torch.from_numpy(b))
+        else:
+            fill_uniform(A, seed=seed * 1000003 + si)
+            fill_uniform(B, seed=seed * 1000003 + si + 7)
+        C = colmajor_empty(m, n, dt, "cuda")
+        impl = "ablation" if variant in (Variant.V0, Variant.V1, Variant.V2) else "auto"
+
+        def call():
+            C.zero_()
+            gemm(A, B, C, variant=variant, params=params, impl=impl, c_is_zero=True)
+
+        ms = _time_ms(call, reps)
+        ref = (A.double() @ B.double()).cpu().numpy()
+        got = C.double().cpu().numpy()
+        err = float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1.0)))
+        fro = float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300))
+        eb = prec.bytes_per_element
+        byts = eb * (m * k + k * n + m * n)
+        pl = tuning.plan(prec.value, m, k, n, impl=impl)
+        gbps = byts / ms / 1e6
+        row = base + [t1, t2, t3, tcf, validate_problem(m, k, n).value, pl["impl"], pl["consumer"],
+                      pl["rows_per_block"], pl["cols_per_pass"], pl["cols_per_stage"], pl["stages"], pl["items"],
+                      pl["grid"], ms, 2.0 * m * k * n / ms / 1e6, gbps, gbps / _hbm_peak(), err, fro, ""]
+        del A, B, C
+        return row
+    except Exception as exc:  # infeasible params etc.: per-row error, keep going (cli.py:155-160)
+        row = base + [override.get("t1"), override.get("t2"), override.get("t3"), override.get("tcf")]
+        row += [""] * (len(RUN_HEADER) - len(row) - 1)
+        return row + [f"{type(exc).__name__}: {exc}"]
+
+
+def cmd_run(prec: Precision, shapes, variants, override, seed, out, reps=10) -> int:
+    rows = [_run_point(prec, sh, v, override, seed, si, reps) for si, sh in enumerate(shapes) for v in variants]
+    _write_csv(out, RUN_HEADER, rows)
+    return 0
+
+
+TUNE_HEADER = ["gpu", "precision", "m", "k", "n", "consumer", "small_kb", "big_kb", "tail_pct", "batch_kb",
+               "time_ms", "is_default", "is_best", "items", "grid", "t1", "t2", "t3"]
+
+
+def cmd_tune(prec: Precision, shape, out, reps=7) -> int:
+    m, k, n = shape
+    r = tuning.tune_tsm2r(m, k, n, prec.value, reps=reps)
+    rows = []
+    for e in r.table:
+        t = e["tuning"]
+        pl = e["plan"]
+        rows.append(["B200", prec.value, m, k, n, tuning.CONSUMERS[t["consumer"]], t["small_kb"], t["big_kb"],
+                     t["tail_pct"], t["batch_kb"], e["ms"], t == tuning.Tuning().__dict__,
+                     t == r.best.__dict__, pl["items"], pl["grid"], pl["t1"], pl["t2"], pl["t3"]])
+    _write_csv(out, TUNE_HEADER, rows)
+    return 0
+
+
+MODEL_HEADER = ["gpu", "precision", "ridge_n", "mem_bandwidth_gbs", "peak_gflops", "m", "k", "n", "bytes",
+                "flops", "time_mem_ms", "time_comp_ms", "bound_class"]
+
+
+def cmd_model(prec: Precision, out) -> int:
+    """B200 roofline per n at the 30720^2 problem (the reference's model table, cli.py:234-253),
+    with the corrected 2-flops-per-FMA ridge and measured peaks."""
+    eb = prec.bytes_per_element
+    bw = B200_SPEC["mem_bandwidth_read_gbs"] * 1e9
+    pk = (B200_SPEC["peak_gflops_double"] if prec is Precision.DOUBLE else B200_SPEC["peak_gflops_single"]) * 1e9
+    ridge = pk / bw * eb / 2
+    rows = []
+    mk = 30720
+    for n in (2, 4, 8, 16, 32):
+        byts = eb * (mk * mk + mk * n + 2 * mk * n)
+        flops = 2.0 * mk * mk * n
+        tm, tc = byts / bw, flops / pk
+        rows.append(["B200", prec.value, ridge, bw / 1e9, pk / 1e9, mk, mk, n, byts, flops, tm * 1e3, tc * 1e3,
+                     "memory" if tm >= tc else "compute"])
+    _write_csv(out, MODEL_HEADER, rows)
+    return 0
+
+
+SWEEP_HEADER = ["gpu", "precision", "m", "k", "n", "batch_kb", "time_ms", "gbps", "is_best"]
+
+
+def cmd_sweep_tcf(prec: Precision, k: int, n: int, out, ms=(10**4, 10**5, 10**6, 10**7), reps=7) -> int:
+    """TSM2L dispatch-granularity sweep (the tcf analogue; reference cli.py:265-297)."""
+    rows = []
+    eb = prec.bytes_per_element
+    for m in ms:
+        r = tuning.select_tcf(m, k, n, prec.value, reps=reps)
+        for e in r.table:
+            t = e["tuning"]
+            byts = eb * (m * k + k * n + 2 * m * n)
+            rows.append(["B200", prec.value, m, k, n, t["batch_kb"], e["ms"], byts / e["ms"] / 1e6,
+                         t == r.best.__dict__])
+    _write_csv(out, SWEEP_HEADER, rows)
+    return 0
+
+
+def build_parser() -> argparse.ArgumentParser:
+    p = argparse.ArgumentParser(prog="tsm2x", description="B200 TSM2X experiments (measured)")
+    sub = p.add_subparsers(dest="command", required=True)
+
+    def common(q):
+        q.add_argument("--gpu", default="B200", help="accepted for reference compatibility; must be B200")
+        q.add_argument("--precision", choices=["single", "double"], default="double")
+        q.add_argument("--out", default=None)
+
+    r = sub.add_parser("run")
+    common(r)
+    for d in ("m", "k", "n"):
+        r.add_argument(f"--{d}", type=int, action="append", required=True)
+    r.add_argument("--variant", action="append", default=None)
+    for f in ("t1", "t2", "t3", "tcf"):
+        r.add_argument(f"--{f}", type=int, default=None)
+    r.add_argument("--seed", type=int, default=0)
+    r.add_argument("--reps", type=int, default=10)
+    t = sub.add_parser("tune")
+    common(t)
+    for d in ("m", "k", "n"):
+        t.add_argument(f"--{d}", type=int, required=True)
+    mo = sub.add_parser("model")
+    common(mo)
+    s = sub.add_parser("sweep-tcf")
+    common(s)
+    s.add_argument("--k", type=int, default=16)
+    s.add_argument("--n", type=int, default=16)
+    return p
+
+
+def _shapes(args) -> List[tuple]:
+    L = max(len(args.m), len(args.k), len(args.n))
+
+    def ex(xs):
+        if len(xs) == 1:
+            return xs * L
+        if len(xs) != L:
+            raise ValueError("--m/--k/--n lists must have equal length (or length 1)")
+        return xs
+    return list(zip(ex(args.m), ex(args.k), ex(args.n)))
+
+
+def main(argv: Optional[Sequence[str]] = None) -> int:
+    args = build_parser().parse_args(argv)
+    prec = Precision.parse(args.precision)
+    try:
+        if args.gpu.upper() != "B200":
+            raise ValueError(f"this front-end measures the local B200; --gpu {args.gpu!r} is not available")
+        if args.command == "run":
+            override = {f: getattr(args, f) for f in ("t1", "t2", "t3", "tcf") if getattr(args, f) is not None}
+            variants = [Variant.parse(v) for v in (args.variant or [])]
+            return cmd_run(prec, _shapes(args), variants, override, args.seed, args.out or "run.csv", args.reps)
+        if args.command == "tune":
+            return cmd_tune(prec, (args.m, args.k, args.n), args.out or "tune.csv")
+        if args.command == "model":
+            return cmd_model(prec, args.out or "model.csv")
+        if args.command == "sweep-tcf":
+            return cmd_sweep_tcf(prec, args.k, args.n, args.out or "sweep_tcf.csv")
+        raise ValueError(f"unknown command {args.command}")
+    except Exception as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return 2
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -348,6 +348,26 @@ struct DmmaConsumer {
   }
 };
 
+// Diagnostic only (TSM2X_CONSUMER=null): touches one element per stage and writes nothing —
+// isolates the cost (time, power) of the TMA pipeline itself from the arithmetic. Results are
+// garbage by design; never selected automatically.
+template <typename T, int NT>
+struct NullConsumer {
+  using Cfg = TmaCfg<T, NT>;
+  static constexpr bool kFragB = false;
+  T sink;
+  int ct;
+  __device__ __forceinline__ void init(int consumer_thread) {
+    ct = consumer_thread;
+    sink = T(0);
+  }
+  __device__ __forceinline__ void zero() {}
+  __device__ __forceinline__ void stage(const T* sA, const T* sB) { sink += sA[ct] * sB[0]; }
+  __device__ __forceinline__ void finish(const DynArgs<T>& a, int64_t rb) const {
+    if (sink == T(12345.678)) a.C[0] = sink;
+  }
+};
+
 template <typename T, int NT, typename Consumer>
 __global__ void __launch_bounds__(TmaCfg<T, NT>::THREADS, 1)
     tsm2r_stream_tma(const DynArgs<T> a, const __grid_constant__ CUtensorMap tmA) {

@@ -286,7 +286,7 @@ static Tuning current_tuning() {
 // Consumer choice (tsm2r_tma.cuh): DMMA for fp64 split row blocks at NT >= 8 (issue slots /
 // power at the FP64-heavy widths), packed FFMA2 for fp32 at NT >= 2, plain FMA otherwise.
 // TSM2X_CONSUMER=fma|dmma|ffma2 in the environment overrides (ablation runs).
-enum ConsumerKind { kFma = 0, kDmma = 1, kFfma2 = 2 };
+enum ConsumerKind { kFma = 0, kDmma = 1, kFfma2 = 2, kNull = 3 };
 
 static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
   static const int env = [] {
@@ -295,8 +295,10 @@ static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
     if (!strcmp(e, "fma")) return (int)kFma;
     if (!strcmp(e, "dmma")) return (int)kDmma;
     if (!strcmp(e, "ffma2")) return (int)kFfma2;
+    if (!strcmp(e, "null")) return (int)kNull;  // diagnostic: pipeline only, wrong results
     return -1;
   }();
+  if (env == kNull) return kNull;
   const int want = env >= 0 ? env : (tu.consumer == 1 ? kFma : tu.consumer == 2 ? kDmma : tu.consumer == 3 ? kFfma2 : -1);
   const bool dmma_ok = eb == 8 && (nt == 8 || nt == 16);
   const bool ffma2_ok = eb == 4 && nt >= 2;
@@ -352,6 +354,10 @@ template <int NT>
 struct ConsumerFor<double, NT, kDmma> {
   using type = typename std::conditional<(NT == 8 || NT == 16), DmmaConsumer<(NT >= 8 ? NT : 8)>,
                                          FmaConsumer<double, NT>>::type;
+};
+template <typename T, int NT>
+struct ConsumerFor<T, NT, kNull> {
+  using type = NullConsumer<T, NT>;
 };
 template <int NT>
 struct ConsumerFor<float, NT, kFfma2> {
@@ -415,6 +421,8 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
     TSM2X_TRY((launch_tma_kernel<T, NT, kDmma>(a, tmap, G, s)));
   else if (kind == kFfma2)
     TSM2X_TRY((launch_tma_kernel<T, NT, kFfma2>(a, tmap, G, s)));
+  else if (kind == kNull)
+    TSM2X_TRY((launch_tma_kernel<T, NT, kNull>(a, tmap, G, s)));
   else
     TSM2X_TRY((launch_tma_kernel<T, NT, kFma>(a, tmap, G, s)));
   if (timed) {
