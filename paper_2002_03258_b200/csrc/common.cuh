@@ -119,6 +119,10 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 
+// Programmatic dependent launch (griddepcontrol): see prep_dyn / tsm2r_stream_tma.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------------------------------------
 // Stream-K partition of U = num_rb * num_kb work units (row block major, k block minor) over G
 // CTAs: CTA g owns units [start(g), start(g+1)), start(g) = floor(g*U/G). Every CTA gets

@@ -387,13 +387,14 @@ __global__ void __launch_bounds__(TmaCfg<T, NT>::THREADS, 1)
       mbar_init(&empty[s], Cfg::CW);
     }
     mbar_fence_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
   }
   __syncthreads();
+  pdl_wait();  // Bt and the zeroed accumulation target come from the prep kernel
 
   if (warp == 0) {
     // ---------------- producer
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
       const uint64_t pol = policy_evict_first();
       int it = 0;
       for (;;) {
@@ -474,6 +475,40 @@ __global__ void prep_bfrag(const double* __restrict__ B, int64_t ldb, int64_t k,
   const int64_t row = 4 * kg + (lane & 3);
   const int col = 8 * nt + (lane >> 2);
   Bf[i] = (row < k && col < w) ? B[row + col * ldb] : 0.0;
+}
+
+// Programmatic dependent launch: the prep kernel lets the stream kernel launch (and run its
+// prologue: barrier init, tensor-map prefetch) while prep is still running; the stream kernel
+// waits for prep's writes (Bt, zeroed accumulator) with griddepcontrol.wait before using them.
+
+// One prep launch per pass of the dynamic kernel: Bt (row-major, or DMMA fragment order when
+// FRAG) and, for split row blocks, the zeroed accumulation target (C itself for fp64 under the
+// zero-C contract, or the fp64 accumulator for fp32) — zrows x zcols at zp with leading dim zld.
+template <typename T, int NT, bool FRAG, typename Z>
+__global__ void prep_dyn(const T* __restrict__ B, int64_t ldb, int64_t k, int64_t kpad, int w, T* __restrict__ Bt,
+                         Z* __restrict__ zp, int64_t zld, int64_t zrows, int zcols) {
+  pdl_launch_dependents();
+  const int64_t nb = kpad * NT, nz = zp ? zrows * zcols : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb + nz; i += stride) {
+    if (i < nb) {
+      if constexpr (FRAG) {
+        const int lane = (int)(i % 32);
+        const int64_t tile = i / 32;
+        const int nt = (int)(tile % (NT / 8));
+        const int64_t row = 4 * (tile / (NT / 8)) + (lane & 3);
+        const int col = 8 * nt + (lane >> 2);
+        Bt[i] = (row < k && col < w) ? B[row + col * ldb] : T(0);
+      } else {
+        const int64_t c = i / NT;
+        const int j = (int)(i - c * NT);
+        Bt[i] = (j < w && c < k) ? B[c + j * ldb] : T(0);
+      }
+    } else {
+      const int64_t z = i - nb, col = z / zrows, row = z - col * zrows;
+      zp[row + col * zld] = Z(0);
+    }
+  }
 }
 
 // fp32 split row blocks: C = (float)((double)C + acc) (or (float)acc under the zero-C contract).

@@ -372,8 +372,18 @@ static int launch_tma_kernel(const DynArgs<T>& a_in, const CUtensorMap& tmap_in,
   TSM2X_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   DynArgs<T> a = a_in;
   alignas(64) CUtensorMap tmap = tmap_in;
-  void* args[] = {&a, &tmap};
-  TSM2X_CUDA(cudaLaunchKernel((const void*)kern, dim3((unsigned)G), dim3(Cfg::THREADS), args, Cfg::SMEM, s));
+  // programmatic dependent launch: overlap this kernel's launch + prologue with prep_dyn
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)G);
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TSM2X_CUDA(cudaLaunchKernelEx(&cfg, kern, a, tmap));
   return check_launch("tsm2r_stream_tma");
 }
 
@@ -400,17 +410,36 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   a.ldacc = (int64_t)it.num_rb * Cfg::R;
   const size_t acc_bytes = (split && sizeof(T) == 4) ? (size_t)a.ldacc * NT * sizeof(double) : 0;
   const int kind = pick_consumer_rt(sizeof(T), NT, split, tu);
-  T* Bt;
-  char* rest;
-  TSM2X_TRY((stage_bt<T, NT>(ws, k, kpad, w, B, ldb, acc_bytes, 8, s, &Bt, &rest, kind == kDmma)));
-  a.Bt = Bt;
-  a.acc = acc_bytes ? reinterpret_cast<double*>(rest) : nullptr;
+  const size_t bt_bytes = align_up((size_t)kpad * NT * sizeof(T), 256);
+  TSM2X_TRY(ws_reserve(ws, bt_bytes + acc_bytes, 8, s));
+  a.Bt = reinterpret_cast<T*>(ws->buf);
+  a.acc = acc_bytes ? reinterpret_cast<double*>(static_cast<char*>(ws->buf) + bt_bytes) : nullptr;
   a.queue = reinterpret_cast<unsigned long long*>(ws->counters);  // zero between launches
-  if (split) {
-    if (sizeof(T) == 4) {
-      TSM2X_CUDA(cudaMemsetAsync(a.acc, 0, acc_bytes, s));
-    } else if (c_is_zero) {
-      TSM2X_CUDA(cudaMemset2DAsync(C, ldc * eb, 0, m * eb, w, s));
+  {
+    // one prep launch: Bt, plus the zeroed accumulation target of split row blocks
+    double* zp = nullptr;
+    int64_t zld = 0, zrows = 0;
+    if (split && sizeof(T) == 4) {
+      zp = a.acc;
+      zld = zrows = a.ldacc;
+    } else if (split && c_is_zero) {
+      zp = reinterpret_cast<double*>(C);
+      zld = ldc;
+      zrows = m;
+    }
+    const int64_t tot = kpad * NT + (zp ? zrows * w : 0);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, (int64_t)di.sms * 16));
+    if constexpr (sizeof(T) == 8 && (NT == 8 || NT == 16)) {
+      if (kind == kDmma) {
+        prep_dyn<T, NT, true, double><<<grid, 256, 0, s>>>(B, ldb, k, kpad, w, const_cast<T*>(a.Bt), zp, zld, zrows, w);
+        TSM2X_TRY(check_launch("prep_dyn"));
+      } else {
+        prep_dyn<T, NT, false, double><<<grid, 256, 0, s>>>(B, ldb, k, kpad, w, const_cast<T*>(a.Bt), zp, zld, zrows, w);
+        TSM2X_TRY(check_launch("prep_dyn"));
+      }
+    } else {
+      prep_dyn<T, NT, false, double><<<grid, 256, 0, s>>>(B, ldb, k, kpad, w, const_cast<T*>(a.Bt), zp, zld, zrows, w);
+      TSM2X_TRY(check_launch("prep_dyn"));
     }
   }
   alignas(64) CUtensorMap tmap;
