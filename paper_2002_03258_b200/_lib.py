@@ -11,7 +11,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtsm2x.so")
+LIB_PATH = os.environ.get("TSM2X_LIB_PATH_EXPERIMENT") or os.path.join(_HERE, "libtsm2x.so")
 
 OK, EINVAL, ECUDA, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4
 FLAG_C_IS_ZERO, FLAG_CHECK_ZERO_C, FLAG_DETERMINISTIC = 0x1, 0x2, 0x4

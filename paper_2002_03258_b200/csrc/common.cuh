@@ -89,7 +89,24 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+#ifndef TSM2X_WAIT_BACKOFF_NS
+#define TSM2X_WAIT_BACKOFF_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if TSM2X_WAIT_BACKOFF_NS > 0
+  while (!mbar_try_wait(bar, parity)) __nanosleep(TSM2X_WAIT_BACKOFF_NS);
+#else
   asm volatile(
       "{\n .reg .pred p;\n"
       "TSM2X_WAIT_%=:\n"
@@ -97,6 +114,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       " @!p bra TSM2X_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 // global -> shared bulk copy completing on an mbarrier; bytes % 16 == 0, both addresses 16B-aligned.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

@@ -49,8 +49,12 @@ struct TmaCfg {
 };
 
 // Item geometry: per row block, nbig chunks of kbig columns over [0, kbig_end), then nsmall
-// chunks of ksmall columns over [kbig_end, k). Ids: all big items (row-block major), then all
-// small items (row-block major). batch > 1 (single-chunk row blocks only) hands out that many
+// chunks of ksmall columns over [kbig_end, k). Ids: all big items, then all small items, each
+// class COLUMN-CHUNK major (row block fastest): the CTAs in flight work on the same columns of
+// neighbouring row blocks, so DRAM sees each column (contiguous in memory) read end to end at
+// about the same time — row-buffer friendly. Row-block-major order read scattered 4 KB pieces
+// and cost ~150 W more at the same bandwidth, which the 1000 W cap turned into SM clock
+// (profiles/README.md). batch > 1 (single-chunk row blocks only) hands out that many
 // consecutive items per queue access.
 struct Items {
   int64_t num_rb;
@@ -62,13 +66,15 @@ struct Items {
   __device__ void decode(int64_t id, int64_t k, int64_t* rb, int64_t* c0, int64_t* c1) const {
     const int64_t n_big_items = num_rb * nbig;
     if (id < n_big_items) {
-      *rb = id / nbig;
-      *c0 = (id - *rb * nbig) * kbig;
+      const int64_t c = id / num_rb;
+      *rb = id - c * num_rb;
+      *c0 = c * kbig;
       *c1 = min64(*c0 + kbig, kbig_end);
     } else {
       const int64_t j = id - n_big_items;
-      *rb = j / nsmall;
-      *c0 = kbig_end + (j - *rb * nsmall) * ksmall;
+      const int64_t c = j / num_rb;
+      *rb = j - c * num_rb;
+      *c0 = kbig_end + c * ksmall;
       *c1 = min64(*c0 + ksmall, k);
     }
   }
@@ -446,12 +452,15 @@ __global__ void __launch_bounds__(TmaCfg<T, NT>::THREADS, 1)
     const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
     mbar_wait(&full[s], ph);
     const longlong2 md = meta[s];
+    if (md.y < 0) {  // end marker (a CTA may get no item at all: test before comparing with cur)
+      if (cur >= 0) cons.finish(a, cur_rb);
+      break;
+    }
     if (md.y != cur) {
       if (cur >= 0) {
         cons.finish(a, cur_rb);
         cons.zero();
       }
-      if (md.y < 0) break;
       cur = md.y;
       cur_rb = md.x;
     }

@@ -108,6 +108,32 @@ def test_aligned_tma_many_shapes(det):
             _check(C.cpu().numpy(), ref, k, "double" if dt == torch.float64 else "single", what=(m, k, n, dt))
 
 
+def test_dynamic_queue_item_counts():
+    """Split shapes whose item count is at / below / just above the CTA count (some CTAs get no
+    item at all — the end-of-work marker must still release them), and tiny single-item ones."""
+    import torch
+    tsm = _tsm()
+    rng = np.random.default_rng(17)
+    for (m, k, n) in [(1024, 1024, 16), (1024, 1024, 8), (512, 300, 8), (1500, 2000, 16), (300, 5000, 4),
+                      (10000, 700, 16), (513, 4000, 9), (64, 129, 1)]:
+        for dt in (torch.float64, torch.float32):
+            A = tsm.colmajor_empty(m, k, dt, "cuda")
+            A.copy_(torch.from_numpy(rng.random((m, k))).to(dt))
+            B = tsm.colmajor_empty(k, n, dt, "cuda")
+            B.copy_(torch.from_numpy(rng.random((k, n))).to(dt))
+            C = tsm.colmajor_empty(m, n, dt, "cuda")
+            C0 = rng.random((m, n))
+            C.copy_(torch.from_numpy(C0).to(dt))
+            for _ in range(3):  # repeated launches reuse the queue / workspace
+                tsm.gemm(A, B, C)
+            torch.cuda.synchronize()
+            An, Bn = A.cpu().numpy(), B.cpu().numpy()
+            ref = C0.astype(An.dtype)
+            for _ in range(3):
+                ref = naive_gemm(An, Bn, ref)
+            _check(C.cpu().numpy(), ref, 3 * k, "double" if dt == torch.float64 else "single", what=(m, k, n, dt))
+
+
 @pytest.mark.parametrize("dt", ["float64", "float32"])
 def test_deterministic_repeat(dt):
     """deterministic=True (static split, fixed-order combine): launches give bitwise-identical C;
@@ -162,6 +188,42 @@ def test_l_opt2_device_check():
     C.zero_()
     tsm.gemm(A, B, C, variant="l-opt2", check_zero_c=True)
     assert torch.all(C == 4.0)
+
+
+@pytest.mark.parametrize("variant", ["v3", "l-opt1", "l-opt2"])
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_run_native_host_path_shapes(variant, prec):
+    """run_native (host Matrix in/out) across TSM2R/TSM2L shapes, both precisions, n > 16,
+    nonzero C (except L_OPT2), including fp32 split row blocks (fp64 accumulator + finalize)."""
+    tsm = _tsm()
+    rng = np.random.default_rng(zlib.crc32(f"{variant}/{prec}".encode()))
+    dt = np.float64 if prec == "double" else np.float32
+    for (m, k, n) in [(5000, 6000, 8), (3001, 9000, 17), (100000, 16, 16), (40000, 40, 3)]:
+        A = rng.random((m, k)).astype(dt)
+        B = rng.random((k, n)).astype(dt)
+        C0 = np.zeros((m, n), dt) if variant == "l-opt2" else rng.random((m, n)).astype(dt)
+        v = tsm.Variant.parse(variant)
+        p = tsm.KernelParams(t1=128, t2=min(4, n), t3=4, tcf=2 if v.is_tsm2l else 1, variant=v)
+        out = tsm.run_native(v, tsm.Matrix.from_2d(A, prec), tsm.Matrix.from_2d(B, prec),
+                             tsm.Matrix.from_2d(C0, prec), p)
+        _check(out.to_2d(), naive_gemm(A, B, C0), k, prec, what=(variant, prec, m, k, n))
+
+
+def test_accepts_reference_objects_duck_typed():
+    """run_native takes objects shaped like the reference's Matrix/KernelParams (rows, cols,
+    storage, precision.value; t1..tcf, variant.value)."""
+    import types
+    tsm = _tsm()
+    rng = np.random.default_rng(9)
+    A, B = rng.random((300, 200)), rng.random((200, 4))
+    prec = types.SimpleNamespace(value="double")
+
+    def mat(X):
+        return types.SimpleNamespace(rows=X.shape[0], cols=X.shape[1], storage=X.reshape(-1, order="F"),
+                                     precision=prec)
+    params = types.SimpleNamespace(t1=128, t2=4, t3=4, tcf=1, variant=types.SimpleNamespace(value="v3"))
+    out = tsm.run_native(types.SimpleNamespace(value="v3"), mat(A), mat(B), mat(np.zeros((300, 4))), params)
+    _check(out.to_2d(), naive_gemm(A, B, np.zeros((300, 4))), 200, "double")
 
 
 def test_wide_n_multi_pass():

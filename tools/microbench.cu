@@ -199,13 +199,20 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&g_buf, bytes)); CK(cudaMemset(g_buf, 0, bytes)); CK(cudaMalloc(&g_sink, 64));
     g_n2 = bytes / 16;
     cudaEvent_t a, b; CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
+    const bool bulk = argc > 2 && std::string(argv[2]) == "bulk";
+    constexpr int ST = 4, CH = 16384;
+    const size_t bsmem = ST * CH + 2 * ST * 8;
+    CK(cudaFuncSetAttribute(read_bulk<ST, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
     for (int i = 0; i < 1000; ++i) {
       if (i == 500) CK(cudaEventRecord(a));
-      read_ldg<8><<<sms * 2, 512>>>(g_buf, g_n2, g_sink);
+      if (bulk)
+        read_bulk<ST, CH><<<sms * 2, 256, bsmem>>>((const char*)g_buf, bytes / CH, g_sink);
+      else
+        read_ldg<8><<<sms * 2, 512>>>(g_buf, g_n2, g_sink);
     }
     CK(cudaEventRecord(b)); CK(cudaEventSynchronize(b));
     float ms; CK(cudaEventElapsedTime(&ms, a, b));
-    printf("{\"test\": \"read_ldg_sustained_2nd_half\", \"GBps\": %.1f}\n", 500.0 * bytes / ms / 1e6);
+    printf("{\"test\": \"read_%s_sustained_2nd_half\", \"GBps\": %.1f}\n", bulk ? "bulk" : "ldg", 500.0 * bytes / ms / 1e6);
     return 0;
   }
   printf("{\"device\": \"%s\", \"sms\": %d, \"l2_bytes\": %d, \"smem_optin\": %zu}\n", prop.name, sms, prop.l2CacheSize, prop.sharedMemPerBlockOptin);
