@@ -1,3 +1,3 @@
 set -x
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -8
-timeout 600 python bench.py 2>&1 | tail -1
+timeout 1200 python tools/abtest.py 6 2>&1 | tail -6
+cp profiles/abtest_r01.json gpurun_out/
