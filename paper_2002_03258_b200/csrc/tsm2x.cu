@@ -305,7 +305,7 @@ static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
   if (want == kFma) return kFma;
   if (want == kDmma) return dmma_ok ? kDmma : kFma;
   if (want == kFfma2) return ffma2_ok ? kFfma2 : kFma;
-  if (dmma_ok && split) return kDmma;
+  if (dmma_ok && split && nt == 16) return kDmma;  // n=8: DFMA sustains higher clocks (profiles/abtest_r01.json)
   if (ffma2_ok) return kFfma2;
   return kFma;
 }
