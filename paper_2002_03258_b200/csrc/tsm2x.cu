@@ -311,13 +311,16 @@ static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
 }
 
 // Item geometry of the dynamic TMA kernel for one pass (rows_per_block = R, KC columns/stage).
-static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, const Tuning& tu, Items* it,
+static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, int nt, const Tuning& tu, Items* it,
                        int64_t* grid) {
   const int64_t G_full = sms;  // one CTA per SM (smem-bound by design)
   it->num_rb = (m + R - 1) / R;
   const double col_bytes = (double)R * eb;  // one column of one row block
   const double per_cta = (double)m * k * eb / (double)G_full;
-  const double small_b = tu.small_kb > 0 ? tu.small_kb * 1024.0 : std::min(512.0 * 1024, std::max(64.0 * 1024, per_cta / 48));
+  // 16-column passes: fewer, larger small items and a shorter small-item tail (fewer fp64
+  // reductions per byte; sustained A/B, profiles/abtest_r01.json)
+  const double small_cap = nt >= 16 ? 1024.0 * 1024 : 512.0 * 1024;
+  const double small_b = tu.small_kb > 0 ? tu.small_kb * 1024.0 : std::min(small_cap, std::max(64.0 * 1024, per_cta / 48));
   const double big_b =
       tu.big_kb > 0 ? std::max(small_b, tu.big_kb * 1024.0) : std::min(4.0 * 1024 * 1024, std::max(small_b, per_cta / 6));
   const int64_t ksmall = std::max<int64_t>(KC, (int64_t)align_up((size_t)(small_b / col_bytes), KC));
@@ -332,7 +335,7 @@ static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, 
     it->ksmall = (int64_t)align_up((size_t)k, KC);
     it->batch = std::max<int64_t>(1, (int64_t)(batch_b / ((double)k * col_bytes)));
   } else {
-    const int pct = tu.tail_pct > 0 ? std::min(tu.tail_pct, 100) : 20;
+    const int pct = tu.tail_pct > 0 ? std::min(tu.tail_pct, 100) : (nt >= 16 ? 10 : 20);
     const int64_t tail_cols = std::max<int64_t>(1, (k * pct + 99) / 100);
     const int64_t tail = std::min<int64_t>(k, (int64_t)align_up((size_t)tail_cols, (size_t)ksmall));
     it->kbig_end = ((k - tail) / KC) * KC;
@@ -404,7 +407,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   a.vec_c = aligned16(C) && (ldc % Vec<T>::N == 0);
   Items& it = a.it;
   int64_t G;
-  make_items(di.sms, m, k, eb, Cfg::R, Cfg::KC, tu, &it, &G);
+  make_items(di.sms, m, k, eb, Cfg::R, Cfg::KC, NT, tu, &it, &G);
   const bool split = it.nch() > 1;
   const int64_t kpad = (int64_t)align_up((size_t)k, Cfg::KC);
   a.ldacc = (int64_t)it.num_rb * Cfg::R;
@@ -1180,7 +1183,7 @@ int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, 
   const Tuning tu = current_tuning();
   Items it;
   int64_t G;
-  make_items(sms, m, k, eb, R, out->cols_per_stage, tu, &it, &G);
+  make_items(sms, m, k, eb, R, out->cols_per_stage, nt, tu, &it, &G);
   out->grid = G;
   out->items = it.total;
   out->nbig = it.nbig;

@@ -293,6 +293,44 @@ def test_config2_sampled_rows(n):
 
 
 @pytest.mark.slow
+def test_config5_per_gpu_shard_sampled():
+    """BASELINE config 5 per GPU (ref m=k=65536, n=8, fp64; 34 GB of A) — the largest single-GPU
+    problem — sampled row slabs against the oracle, plus a rank-1 shard of the 2-GPU split
+    generated with its global row offset (what each rank of the multi-GPU run computes)."""
+    import torch
+    from oracle.rng import uniform_block
+    tsm = _tsm()
+    m = k = 65536
+    n = 8
+    A = tsm.colmajor_empty(m, k, torch.float64, "cuda")
+    tsm.fill_uniform(A, seed=5)
+    B = tsm.colmajor_empty(k, n, torch.float64, "cuda")
+    tsm.fill_uniform(B, seed=6)
+    C = tsm.colmajor_empty(m, n, torch.float64, "cuda")
+    C.zero_()
+    tsm.gemm(A, B, C, c_is_zero=True)
+    torch.cuda.synchronize()
+    Ch = C.cpu().numpy()
+    del A
+    torch.cuda.empty_cache()
+    Bh = uniform_block(range(k), range(n), 6)
+    for r0 in (0, 40000, m - 128):
+        rows = range(r0, r0 + 128)
+        ref = naive_gemm(uniform_block(rows, range(k), 5), Bh, np.zeros((128, n)))
+        _check(Ch[r0:r0 + 128], ref, k, "double", what=("config5", r0))
+    # the second half as its own shard (global row offset) agrees with the full run's rows
+    from paper_2002_03258_b200.multi import row_partition
+    s0, s1 = row_partition(m, 2, 1)
+    As = tsm.colmajor_empty(s1 - s0, k, torch.float64, "cuda")
+    tsm.fill_uniform(As, seed=5, row_offset=s0)
+    Cs = tsm.colmajor_empty(s1 - s0, n, torch.float64, "cuda")
+    Cs.zero_()
+    tsm.gemm(As, B, Cs, c_is_zero=True, deterministic=True)
+    torch.cuda.synchronize()
+    _check(Cs.cpu().numpy(), Ch[s0:s1], k, "double", what="shard")
+
+
+@pytest.mark.slow
 def test_config3_tsm2l_sampled():
     import torch
     from oracle.rng import uniform_block
