@@ -64,8 +64,9 @@ typedef struct tsm2x_params {
 #define TSM2X_FLAG_C_IS_ZERO 0x1u   /* caller guarantees C == 0: C is written, never read  */
 #define TSM2X_FLAG_CHECK_ZERO_C 0x2u/* tsm2x_run + L_OPT2: verify C == 0 on the device
                                        (synchronises the stream); EINVAL if not          */
-#define TSM2X_FLAG_DETERMINISTIC 0x4u/* bitwise run-to-run reproducible combine (static split,
-                                       fixed-order sums); default: dynamic, fp64 atomics  */
+#define TSM2X_FLAG_DETERMINISTIC 0x4u/* bitwise run-to-run reproducible: split row blocks are
+                                       combined in column order (per-row-block tickets)
+                                       instead of with fp64 atomics (the default)          */
 
 /* Kernel implementation override (tsm2x_run_ex); AUTO uses the B200 tuning table. */
 enum tsm2x_impl {
@@ -116,6 +117,8 @@ typedef struct tsm2x_tuning {
   int32_t big_kb;     /* KB of A per "big" work item                                          */
   int32_t tail_pct;   /* % of each row block's columns handed out as small items              */
   int32_t batch_kb;   /* single-chunk row blocks (TSM2L): KB of A per queue grab (tcf analogue) */
+  int32_t combine;    /* split row blocks: 0 auto (atomics; ordered if DETERMINISTIC), 1 chunk-ordered,
+                         2 fp64 atomics, 3 static stream-K split (reproducible)                 */
 } tsm2x_tuning;
 int tsm2x_set_tuning(const tsm2x_tuning* t); /* NULL restores the defaults */
 int tsm2x_get_tuning(tsm2x_tuning* out);

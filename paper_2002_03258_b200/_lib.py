@@ -39,7 +39,7 @@ class Tuning(ctypes.Structure):
     """struct tsm2x_tuning (B200 parameter selection knobs; 0 = default)."""
 
     _fields_ = [("consumer", ctypes.c_int32), ("small_kb", ctypes.c_int32), ("big_kb", ctypes.c_int32),
-                ("tail_pct", ctypes.c_int32), ("batch_kb", ctypes.c_int32)]
+                ("tail_pct", ctypes.c_int32), ("batch_kb", ctypes.c_int32), ("combine", ctypes.c_int32)]
 
 
 class Plan(ctypes.Structure):

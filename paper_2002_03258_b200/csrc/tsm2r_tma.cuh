@@ -25,6 +25,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <new>
+
 #include "common.cuh"
 #include "tsm2r_stream.cuh"
 
@@ -63,6 +65,11 @@ struct Items {
   int64_t total;
   int64_t batch;
   __host__ __device__ int64_t nch() const { return nbig + nsmall; }
+  // column-chunk index (0 .. nch-1, increasing with the columns) of an item
+  __device__ int64_t chunk(int64_t id) const {
+    const int64_t n_big_items = num_rb * nbig;
+    return id < n_big_items ? id / num_rb : nbig + (id - n_big_items) / num_rb;
+  }
   __device__ void decode(int64_t id, int64_t k, int64_t* rb, int64_t* c0, int64_t* c1) const {
     const int64_t n_big_items = num_rb * nbig;
     if (id < n_big_items) {
@@ -89,8 +96,11 @@ struct DynArgs {
   int w;            // valid columns in this pass (<= NT)
   int c_is_zero;    // single-chunk row blocks: C is written, never read
   int vec_c;        // C columns 16-B aligned (vector stores allowed)
-  double* acc;      // split row blocks, fp32: fp64 accumulator [NT][ldacc] (zeroed); fp64: null (C)
+  double* acc;      // reduction combine, fp32: fp64 accumulator [NT][ldacc] (zeroed); fp64: null (C)
   int64_t ldacc;
+  int ordered;      // split row blocks: 1 = chunk-ordered combine through per-row-block tickets
+                    // (deterministic), 0 = fp64 atomic reductions
+  unsigned* tickets;  // [num_rb] next chunk allowed to update the row block; zero between launches
   Items it;
   unsigned long long* queue;  // [0] next item, [1] low 32 bits: producers finished
 };
@@ -114,22 +124,60 @@ struct ConsumerSync {
   }
 };
 
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Ordered combine of split row blocks: chunk c of row block rb may update C only after chunks
+// 0..c-1 did (ticket == c), so C's rows receive their partial sums in column order whatever
+// CTA ran which item — bitwise reproducible. Column-chunk-major dispatch hands chunk c of a row
+// block out ~one round of items before chunk c+1, so the wait is almost never taken, and the
+// consumers' pause is absorbed by the TMA ring (the producer keeps streaming).
+struct TicketGuard {
+  const unsigned* t;
+  unsigned c;
+  bool leader;
+  __device__ __forceinline__ TicketGuard(const unsigned* tick, unsigned chunk, bool lead)
+      : t(tick), c(chunk), leader(lead) {
+    if (leader)
+      while (ld_acquire(t) != c) __nanosleep(128);
+    ConsumerSync()();
+  }
+  __device__ __forceinline__ void release(unsigned* tick, unsigned next) const {
+    ConsumerSync()();
+    if (leader) st_release(tick, next);
+  }
+};
+
 // Epilogue of one item. Consumer thread ct owns rows ct + 256*r (r < RPT) of the row block, so
 // every warp-wide access below touches 32 consecutive elements of a C column: coalesced stores
 // for single-chunk row blocks (C (+)= acc), coalesced fp64 reductions for split row blocks
 // (into C for fp64, into the fp64 accumulator for fp32).
 template <typename T, int NT, int RPT, int R>
-__device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int ct, const T (&acc)[RPT][NT]) {
+__device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int64_t item, int ct,
+                                            const T (&acc)[RPT][NT]) {
   const int64_t row_base = rb * R + ct;
-  if (a.it.nch() == 1) {
-    // all loads of C first (one round trip, not NT*RPT dependent ones), then the stores
+  const int64_t nch = a.it.nch();
+  const int64_t c = nch == 1 ? 0 : a.it.chunk(item);
+  if (nch == 1 || a.ordered) {
+    TicketGuard* g = nullptr;
+    alignas(TicketGuard) unsigned char gbuf[sizeof(TicketGuard)];
+    if (nch > 1) g = new (gbuf) TicketGuard(a.tickets + rb, (unsigned)c, ct == 0);
+    // all loads of C first (one round trip, not NT*RPT dependent ones), then the stores; the
+    // first chunk starts from C's input (or from zero under the zero-C contract)
+    const bool read_c = c > 0 || !a.c_is_zero;
     T old[RPT][NT];
 #pragma unroll
     for (int j = 0; j < NT; ++j)
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
         const int64_t row = row_base + r * TmaCfg<T, NT>::BOX;
-        old[r][j] = (!a.c_is_zero && j < a.w && row < a.m) ? __ldcs(a.C + j * a.ldc + row) : T(0);
+        old[r][j] = (read_c && j < a.w && row < a.m) ? __ldcg(a.C + j * a.ldc + row) : T(0);
       }
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
@@ -138,9 +186,15 @@ __device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
         const int64_t row = row_base + r * TmaCfg<T, NT>::BOX;
-        if (row < a.m) __stcs(cj + row, old[r][j] + acc[r][j]);
+        if (row < a.m) {
+          if (nch == 1)
+            __stcs(cj + row, old[r][j] + acc[r][j]);
+          else
+            __stcg(cj + row, old[r][j] + acc[r][j]);
+        }
       }
     }
+    if (g) g->release(a.tickets + rb, c + 1 == nch ? 0u : (unsigned)(c + 1));
     return;
   }
 #pragma unroll
@@ -208,8 +262,8 @@ struct FmaConsumer {
         for (int j = 0; j < NT; ++j) acc[r][j] = fma(av[r], b[j], acc[r][j]);
     }
   }
-  __device__ __forceinline__ void finish(const DynArgs<T>& a, int64_t rb) const {
-    finish_item<T, NT, RPT, Cfg::R>(a, rb, ct, acc);
+  __device__ __forceinline__ void finish(const DynArgs<T>& a, int64_t rb, int64_t item) const {
+    finish_item<T, NT, RPT, Cfg::R>(a, rb, item, ct, acc);
   }
 };
 
@@ -253,13 +307,13 @@ struct Ffma2Consumer {
         for (int p = 0; p < NT / 2; ++p) asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[r][p]) : "l"(a2[r]), "l"(b2[p]));
     }
   }
-  __device__ __forceinline__ void finish(const DynArgs<float>& a, int64_t rb) const {
+  __device__ __forceinline__ void finish(const DynArgs<float>& a, int64_t rb, int64_t item) const {
     float out[RPT][NT];
 #pragma unroll
     for (int r = 0; r < RPT; ++r)
 #pragma unroll
       for (int p = 0; p < NT / 2; ++p) asm("mov.b64 {%0, %1}, %2;" : "=f"(out[r][2 * p]), "=f"(out[r][2 * p + 1]) : "l"(acc[r][p]));
-    finish_item<float, NT, RPT, Cfg::R>(a, rb, ct, out);
+    finish_item<float, NT, RPT, Cfg::R>(a, rb, item, ct, out);
   }
 };
 
@@ -314,10 +368,33 @@ struct DmmaConsumer {
     }
   }
   // accumulator (q, mt, nt, e) holds row 64w + 16q + 2g + mt, column 8nt + 2t + e
-  __device__ __forceinline__ void finish(const DynArgs<double>& a, int64_t rb) const {
+  __device__ __forceinline__ void finish(const DynArgs<double>& a, int64_t rb, int64_t item) const {
     const int g = lane >> 2, t = lane & 3;
     const int64_t base = rb * Cfg::R + 64 * warp + 2 * g;
-    const bool split = a.it.nch() > 1;
+    const int64_t nch = a.it.nch();
+    const int64_t c = nch == 1 ? 0 : a.it.chunk(item);
+    const bool rmw = nch == 1 || a.ordered;
+    if (!rmw) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int64_t row = base + 16 * q + mt;
+          if (row >= a.m) continue;
+#pragma unroll
+          for (int nt = 0; nt < NTI; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int j = 8 * nt + 2 * t + e;
+              if (j < a.w) red_add(a.C + j * a.ldc + row, acc[q][mt][nt][e]);
+            }
+        }
+      return;
+    }
+    TicketGuard* gd = nullptr;
+    alignas(TicketGuard) unsigned char gbuf[sizeof(TicketGuard)];
+    if (nch > 1) gd = new (gbuf) TicketGuard(a.tickets + rb, (unsigned)c, warp == 0 && lane == 0);
+    const bool read_c = c > 0 || !a.c_is_zero;
     double old[4][2][NTI][2];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -329,8 +406,7 @@ struct DmmaConsumer {
           for (int e = 0; e < 2; ++e) {
             const int64_t row = base + 16 * q + mt;
             const int j = 8 * nt + 2 * t + e;
-            old[q][mt][nt][e] =
-                (!split && !a.c_is_zero && row < a.m && j < a.w) ? a.C[j * a.ldc + row] : 0.0;
+            old[q][mt][nt][e] = (read_c && row < a.m && j < a.w) ? __ldcg(a.C + j * a.ldc + row) : 0.0;
           }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -343,14 +419,10 @@ struct DmmaConsumer {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int j = 8 * nt + 2 * t + e;
-            if (j >= a.w) continue;
-            double* c = a.C + j * a.ldc + row;
-            if (split)
-              red_add(c, acc[q][mt][nt][e]);
-            else
-              *c = old[q][mt][nt][e] + acc[q][mt][nt][e];
+            if (j < a.w) __stcg(a.C + j * a.ldc + row, old[q][mt][nt][e] + acc[q][mt][nt][e]);
           }
       }
+    if (gd) gd->release(a.tickets + rb, c + 1 == nch ? 0u : (unsigned)(c + 1));
   }
 };
 
@@ -369,7 +441,7 @@ struct NullConsumer {
   }
   __device__ __forceinline__ void zero() {}
   __device__ __forceinline__ void stage(const T* sA, const T* sB) { sink += sA[ct] * sB[0]; }
-  __device__ __forceinline__ void finish(const DynArgs<T>& a, int64_t rb) const {
+  __device__ __forceinline__ void finish(const DynArgs<T>& a, int64_t rb, int64_t item) const {
     if (sink == T(12345.678)) a.C[0] = sink;
   }
 };
@@ -453,12 +525,12 @@ __global__ void __launch_bounds__(TmaCfg<T, NT>::THREADS, 1)
     mbar_wait(&full[s], ph);
     const longlong2 md = meta[s];
     if (md.y < 0) {  // end marker (a CTA may get no item at all: test before comparing with cur)
-      if (cur >= 0) cons.finish(a, cur_rb);
+      if (cur >= 0) cons.finish(a, cur_rb, cur);
       break;
     }
     if (md.y != cur) {
       if (cur >= 0) {
-        cons.finish(a, cur_rb);
+        cons.finish(a, cur_rb, cur);
         cons.zero();
       }
       cur = md.y;

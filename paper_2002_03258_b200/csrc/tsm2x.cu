@@ -275,6 +275,8 @@ struct Tuning {
   int big_kb = 0;     // A bytes per big item (KB);   default min(4096, max(small, per-CTA share / 6))
   int tail_pct = 0;   // % of each row block's columns dispatched as small items; default 20
   int batch_kb = 0;   // single-chunk row blocks (TSM2L): A bytes per queue grab (tcf analogue); default 1024
+  int combine = 0;    // split row blocks: 0 auto (fp64 atomics; chunk-ordered when DETERMINISTIC is asked),
+                      // 1 chunk-ordered via tickets (bitwise reproducible), 2 fp64 atomics, 3 static split
 };
 static std::mutex g_tune_mu;
 static Tuning g_tune;
@@ -393,7 +395,8 @@ static int launch_tma_kernel(const DynArgs<T>& a_in, const CUtensorMap& tmap_in,
 // TMA flavour, dynamic items (tsm2r_tma.cuh): item sizes from the per-CTA share of the work.
 template <typename T, int NT>
 static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k, int w, const T* A, int64_t lda,
-                         const T* B, int64_t ldb, T* C, int64_t ldc, bool c_is_zero, cudaStream_t s) {
+                         const T* B, int64_t ldb, T* C, int64_t ldc, bool c_is_zero, bool ordered,
+                         cudaStream_t s) {
   using Cfg = TmaCfg<T, NT>;
   const size_t eb = sizeof(T);
   const Tuning tu = current_tuning();
@@ -411,10 +414,13 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   const bool split = it.nch() > 1;
   const int64_t kpad = (int64_t)align_up((size_t)k, Cfg::KC);
   a.ldacc = (int64_t)it.num_rb * Cfg::R;
-  const size_t acc_bytes = (split && sizeof(T) == 4) ? (size_t)a.ldacc * NT * sizeof(double) : 0;
+  a.ordered = ordered ? 1 : 0;
+  const bool atomic_split = split && !a.ordered;
+  const size_t acc_bytes = (atomic_split && sizeof(T) == 4) ? (size_t)a.ldacc * NT * sizeof(double) : 0;
   const int kind = pick_consumer_rt(sizeof(T), NT, split, tu);
   const size_t bt_bytes = align_up((size_t)kpad * NT * sizeof(T), 256);
-  TSM2X_TRY(ws_reserve(ws, bt_bytes + acc_bytes, 8, s));
+  TSM2X_TRY(ws_reserve(ws, bt_bytes + acc_bytes, (size_t)it.num_rb + 8, s));
+  a.tickets = reinterpret_cast<unsigned*>(ws->counters + 8);  // zero between launches
   a.Bt = reinterpret_cast<T*>(ws->buf);
   a.acc = acc_bytes ? reinterpret_cast<double*>(static_cast<char*>(ws->buf) + bt_bytes) : nullptr;
   a.queue = reinterpret_cast<unsigned long long*>(ws->counters);  // zero between launches
@@ -422,10 +428,10 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
     // one prep launch: Bt, plus the zeroed accumulation target of split row blocks
     double* zp = nullptr;
     int64_t zld = 0, zrows = 0;
-    if (split && sizeof(T) == 4) {
+    if (atomic_split && sizeof(T) == 4) {
       zp = a.acc;
       zld = zrows = a.ldacc;
-    } else if (split && c_is_zero) {
+    } else if (atomic_split && c_is_zero) {
       zp = reinterpret_cast<double*>(C);
       zld = ldc;
       zrows = m;
@@ -461,7 +467,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
     TSM2X_CUDA(cudaEventRecord(t_ev_stop, s));
     t_ev_start = t_ev_stop = nullptr;
   }
-  if (split && sizeof(T) == 4) {
+  if (atomic_split && sizeof(T) == 4) {
     const int64_t tot = m * w;
     const unsigned grid = (unsigned)std::min<int64_t>((tot + 255) / 256, (int64_t)di.sms * 8);
     tsm2_finalize<T><<<grid, 256, 0, s>>>(a.acc, a.ldacc, C, ldc, m, w, a.c_is_zero);
@@ -598,8 +604,14 @@ static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m,
   const bool tma_ok = aligned16(A) && ((lda * (int64_t)sizeof(T)) % 16 == 0) && m < (int64_t(1) << 31) &&
                       k < (int64_t(1) << 31);
   const bool tma = (impl == TSM2X_IMPL_AUTO || impl == TSM2X_IMPL_STREAM_TMA) && tma_ok;
-  if (tma && deterministic) return run_tsm2r_tma_static<T, NT>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, s);
-  if (tma) return run_tsm2r_tma<T, NT>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, s);
+  // combine of split row blocks: fp64 atomics by default (fastest, sustained A/B in
+  // profiles/abtest_r01.json); DETERMINISTIC (or tuning.combine = 1) selects the chunk-ordered
+  // ticket combine — bitwise reproducible, same dynamic balance and DRAM order, 5-30 % slower;
+  // tuning.combine = 3 the static stream-K split (reproducible too, kept for comparison)
+  const int combine = current_tuning().combine;
+  if (tma && combine == 3) return run_tsm2r_tma_static<T, NT>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, s);
+  const bool ordered = combine == 1 || (combine == 0 && deterministic);
+  if (tma) return run_tsm2r_tma<T, NT>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
   return run_tsm2r_ldg<T, NT>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, s);
 }
 
@@ -1110,8 +1122,9 @@ int tsm2x_set_tuning(const tsm2x_tuning* t) {
   Tuning nt;
   if (t) {
     if (t->consumer < 0 || t->consumer > 3 || t->small_kb < 0 || t->big_kb < 0 || t->tail_pct < 0 ||
-        t->tail_pct > 100 || t->batch_kb < 0)
+        t->tail_pct > 100 || t->batch_kb < 0 || t->combine < 0 || t->combine > 3)
       return fail(TSM2X_EINVAL, "bad tuning values");
+    nt.combine = t->combine;
     nt.consumer = t->consumer;
     nt.small_kb = t->small_kb;
     nt.big_kb = t->big_kb;
@@ -1131,6 +1144,7 @@ int tsm2x_get_tuning(tsm2x_tuning* out) {
   out->big_kb = t.big_kb;
   out->tail_pct = t.tail_pct;
   out->batch_kb = t.batch_kb;
+  out->combine = t.combine;
   return TSM2X_OK;
 }
 
@@ -1173,7 +1187,8 @@ int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, 
   out->rows_per_block = R;
   out->cols_per_stage = TmaCfg<double, 1>::KC;
   out->stages = TmaCfg<double, 1>::STAGES;
-  if (determ) {
+  const Tuning tu0 = current_tuning();
+  if (tu0.combine == 3) {
     out->deterministic = 1;
     out->consumer = 1;
     const int64_t units = ((m + R - 1) / R) * ((k + 7) / 8);
@@ -1192,6 +1207,7 @@ int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, 
   out->ksmall = it.ksmall;
   out->batch = it.batch;
   out->consumer = 1 + pick_consumer_rt(eb, nt, it.nch() > 1, tu);
+  out->deterministic = (it.nch() == 1 || tu.combine == 1 || (tu.combine == 0 && determ)) ? 1 : 0;
   return TSM2X_OK;
 }
 

@@ -103,9 +103,10 @@ def gemm(A, B, C, *, variant=Variant.V3, params=None, c_is_zero: bool = False, i
          stream=None, check_zero_c: bool = False, deterministic: bool = False):
     """In place on device: ``C (+)= A @ B`` for column-major CUDA tensors (fp32 or fp64).
 
-    ``c_is_zero`` elides the read of C (the L_OPT2 contract). ``deterministic`` selects the
-    static-split kernel whose result is bitwise reproducible run to run (the default dynamic
-    kernel combines split row blocks with fp64 atomics: same tolerance, last-bit variation).
+    ``c_is_zero`` elides the read of C (the L_OPT2 contract). ``deterministic`` makes the result
+    bitwise reproducible run to run: row blocks split across CTAs are then combined in column
+    order through per-row-block tickets instead of with fp64 atomics (same tolerance either way;
+    the atomic default is faster).
     Stream-ordered on ``stream`` (default: torch's current stream); returns C.
     """
     import torch

@@ -40,11 +40,14 @@ IMPLS = {v: k for k, v in _lib.IMPL.items()}
 # The library's built-in defaults (tsm2x.cu make_items / pick_consumer_rt), stated here for
 # reporting; 0 in a Tuning means "use these".
 B200_DEFAULTS = {
-    "consumer": "auto: DMMA for fp64 split row blocks at n in {8,16}; FFMA2 for fp32 n >= 2; else FMA",
-    "small_kb": "min(512, max(64, per-CTA share / 48))",
+    "consumer": "auto: DMMA for fp64 split row blocks with 16-column passes; FFMA2 for fp32 n >= 2; else FMA "
+                "(DFMA beats DMMA at n=8 under the power cap: profiles/abtest_r01.json)",
+    "small_kb": "min(512 (1024 for 16-column passes), max(64, per-CTA share / 48))",
     "big_kb": "min(4096, max(small, per-CTA share / 6))",
-    "tail_pct": 20,
+    "tail_pct": "20 (10 for 16-column passes)",
     "batch_kb": 1024,
+    "combine": "fp64 atomics; deterministic=True -> chunk-ordered through per-row-block tickets (bitwise "
+               "reproducible, 5-30 % slower); 3 = static stream-K split",
 }
 
 
@@ -55,9 +58,10 @@ class Tuning:
     big_kb: int = 0
     tail_pct: int = 0
     batch_kb: int = 0
+    combine: int = 0  # split row blocks: 0 auto (atomics; ordered if deterministic), 1 chunk-ordered, 2 atomics, 3 static
 
     def _c(self) -> _lib.Tuning:
-        return _lib.Tuning(self.consumer, self.small_kb, self.big_kb, self.tail_pct, self.batch_kb)
+        return _lib.Tuning(self.consumer, self.small_kb, self.big_kb, self.tail_pct, self.batch_kb, self.combine)
 
 
 def set_tuning(t: Optional[Tuning]) -> None:
@@ -69,7 +73,7 @@ def set_tuning(t: Optional[Tuning]) -> None:
 def get_tuning() -> Tuning:
     out = _lib.Tuning()
     _lib.check(_lib.load().tsm2x_get_tuning(ctypes.byref(out)))
-    return Tuning(out.consumer, out.small_kb, out.big_kb, out.tail_pct, out.batch_kb)
+    return Tuning(out.consumer, out.small_kb, out.big_kb, out.tail_pct, out.batch_kb, out.combine)
 
 
 def plan(precision: str, m: int, k: int, n: int, lda: Optional[int] = None, aligned: bool = True,

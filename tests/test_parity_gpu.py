@@ -146,6 +146,7 @@ def test_deterministic_repeat(dt):
     tsm.fill_uniform(A, seed=11)
     B = tsm.colmajor_empty(k, n, dtype, "cuda")
     tsm.fill_uniform(B, seed=12)
+    from paper_2002_03258_b200 import tuning
     outs = []
     for det in (True, True, True, False):
         C = tsm.colmajor_empty(m, n, dtype, "cuda")
@@ -154,6 +155,22 @@ def test_deterministic_repeat(dt):
         outs.append(C.cpu().numpy())
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
     _check(outs[3], outs[0].astype(np.float64), k, "double" if dt == "float64" else "single")
+    # the static stream-K split (combine=3) is reproducible too; chunk-ordered (combine=1) is
+    # what deterministic=True selects
+    try:
+        for combine in (3, 1):
+            tuning.set_tuning(tuning.Tuning(combine=combine))
+            rep = []
+            for _ in range(2):
+                C = tsm.colmajor_empty(m, n, dtype, "cuda")
+                C.fill_(1.0)
+                tsm.gemm(A, B, C)
+                rep.append(C.cpu().numpy())
+            assert np.array_equal(rep[0], rep[1]), combine
+            _check(rep[0], outs[0].astype(np.float64), k, "double" if dt == "float64" else "single")
+        assert np.array_equal(rep[0], outs[0])  # combine=1 is what deterministic=True runs
+    finally:
+        tuning.set_tuning(None)
 
 
 def test_fill_uniform_matches_host_rng():

@@ -14,10 +14,8 @@ from paper_2002_03258_b200 import tuning  # noqa: E402
 
 T = tuning.Tuning
 CASES = {
-    "r8": ((30720, 30720, 8, torch.float64), [T(), T(consumer=1), T(consumer=2), T(consumer=1, big_kb=1024), T(consumer=1, tail_pct=10)]),
-    "r16": ((30720, 30720, 16, torch.float64), [T(), T(consumer=1), T(consumer=2), T(small_kb=1024, tail_pct=10)]),
-    "f16": ((32768, 32768, 16, torch.float32), [T(), T(tail_pct=10), T(consumer=1)]),
-    "r2": ((30720, 30720, 2, torch.float64), [T(), T(consumer=1), T(small_kb=128, tail_pct=35)]),
+    "r8": ((30720, 30720, 8, torch.float64), [T(), T(combine=1), T(combine=3)]),
+    "f16": ((32768, 32768, 16, torch.float32), [T(), T(combine=1), T(combine=3)]),
 }
 
 
