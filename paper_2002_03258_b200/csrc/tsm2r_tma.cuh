@@ -32,15 +32,17 @@
 
 namespace tsm2x {
 
-template <typename T, int NT>
+template <typename T, int NT, int RPT_ = Vec<T>::N, int CW_ = 8>
 struct TmaCfg {
-  static constexpr int CW = 8;                        // consumer warps
+  static constexpr int CW = CW_;                      // consumer warps
+  static constexpr int CT = 32 * CW;                  // consumer threads
   static constexpr int THREADS = 32 * (CW + 1);       // + producer warp
-  static constexpr int RPT = Vec<T>::N;               // rows per consumer thread
-  static constexpr int R = CW * 32 * RPT;             // rows per row block (512 fp64 / 1024 fp32)
+  static constexpr int RPT = RPT_;                    // rows per consumer thread (one per TMA box)
+  static constexpr int R = CT * RPT;                  // rows per row block (512 fp64 / 1024 fp32)
   static constexpr int BOX = 256;                     // rows per TMA box (box dim limit)
   static constexpr int NBOX = R / BOX;
-  static constexpr int KC = 8;                        // columns per stage
+  static constexpr int KC = 32768 / (R * (int)sizeof(T));  // columns per 32 KB stage (8 by default)
+  static_assert(KC >= 1 && (KC * NT * (int)sizeof(T)) % 16 == 0, "bulk-copy granularity");
   static constexpr int STAGES = 6;
   static constexpr int A_ELEMS = R * KC;
   static constexpr int B_ELEMS = KC * NT;
@@ -118,9 +120,9 @@ __device__ __forceinline__ void red_add(double* p, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
-struct ConsumerSync {
+struct ConsumerSync {  // named barrier over the consumer warps (every warp but the producer)
   __device__ __forceinline__ void operator()() const {
-    asm volatile("bar.sync 1, %0;" ::"r"(TmaCfg<double, 1>::CW * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(blockDim.x - 32) : "memory");
   }
 };
 
@@ -158,7 +160,7 @@ struct TicketGuard {
 // every warp-wide access below touches 32 consecutive elements of a C column: coalesced stores
 // for single-chunk row blocks (C (+)= acc), coalesced fp64 reductions for split row blocks
 // (into C for fp64, into the fp64 accumulator for fp32).
-template <typename T, int NT, int RPT, int R>
+template <typename T, int NT, int RPT, int R, int CT = 256>
 __device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int64_t item, int ct,
                                             const T (&acc)[RPT][NT]) {
   const int64_t row_base = rb * R + ct;
@@ -176,7 +178,7 @@ __device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int
     for (int j = 0; j < NT; ++j)
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
-        const int64_t row = row_base + r * TmaCfg<T, NT>::BOX;
+        const int64_t row = row_base + r * CT;
         old[r][j] = (read_c && j < a.w && row < a.m) ? __ldcg(a.C + j * a.ldc + row) : T(0);
       }
 #pragma unroll
@@ -185,7 +187,7 @@ __device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int
       T* cj = a.C + j * a.ldc;
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
-        const int64_t row = row_base + r * TmaCfg<T, NT>::BOX;
+        const int64_t row = row_base + r * CT;
         if (row < a.m) {
           if (nch == 1)
             __stcs(cj + row, old[r][j] + acc[r][j]);
@@ -202,7 +204,7 @@ __device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int
     if (j >= a.w) continue;
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
-      const int64_t row = row_base + r * TmaCfg<T, NT>::BOX;
+      const int64_t row = row_base + r * CT;
       if constexpr (sizeof(T) == 8) {
         if (row < a.m) red_add(reinterpret_cast<double*>(a.C) + j * a.ldc + row, (double)acc[r][j]);
       } else {
@@ -218,9 +220,9 @@ __device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int
 
 // FMA: thread ct owns rows ct + 256*r; one scalar LDS per row per column (32 consecutive
 // elements per warp, conflict-free), Bt row as broadcast LDS.128s, NT FMAs per row per column.
-template <typename T, int NT>
+template <typename T, int NT, int RPT_ = Vec<T>::N, int CW_ = 8>
 struct FmaConsumer {
-  using Cfg = TmaCfg<T, NT>;
+  using Cfg = TmaCfg<T, NT, RPT_, CW_>;
   using V = typename Vec<T>::type;
   static constexpr int RPT = Cfg::RPT;
   static constexpr bool kFragB = false;
@@ -237,12 +239,14 @@ struct FmaConsumer {
       for (int j = 0; j < NT; ++j) acc[r][j] = T(0);
   }
   __device__ __forceinline__ void stage(const T* sA, const T* sB) {
-    const T* As = sA + ct;
 #pragma unroll
     for (int cc = 0; cc < Cfg::KC; ++cc) {
       T av[RPT];
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) av[r] = As[r * (Cfg::BOX * Cfg::KC) + cc * Cfg::BOX];
+      for (int r = 0; r < RPT; ++r) {
+        const int row = ct + r * Cfg::CT;  // row in the block -> (TMA box, offset in the box)
+        av[r] = sA[(row / Cfg::BOX) * (Cfg::BOX * Cfg::KC) + cc * Cfg::BOX + row % Cfg::BOX];
+      }
       T b[NT];
       if constexpr (NT * sizeof(T) >= 16) {
         constexpr int PER = 16 / (int)sizeof(T);
@@ -263,7 +267,7 @@ struct FmaConsumer {
     }
   }
   __device__ __forceinline__ void finish(const DynArgs<T>& a, int64_t rb, int64_t item) const {
-    finish_item<T, NT, RPT, Cfg::R>(a, rb, item, ct, acc);
+    finish_item<T, NT, RPT, Cfg::R, Cfg::CT>(a, rb, item, ct, acc);
   }
 };
 
@@ -429,9 +433,9 @@ struct DmmaConsumer {
 // Diagnostic only (TSM2X_CONSUMER=null): touches one element per stage and writes nothing —
 // isolates the cost (time, power) of the TMA pipeline itself from the arithmetic. Results are
 // garbage by design; never selected automatically.
-template <typename T, int NT>
+template <typename T, int NT, int RPT_ = Vec<T>::N, int CW_ = 8>
 struct NullConsumer {
-  using Cfg = TmaCfg<T, NT>;
+  using Cfg = TmaCfg<T, NT, RPT_, CW_>;
   static constexpr bool kFragB = false;
   T sink;
   int ct;
@@ -447,9 +451,9 @@ struct NullConsumer {
 };
 
 template <typename T, int NT, typename Consumer>
-__global__ void __launch_bounds__(TmaCfg<T, NT>::THREADS, 1)
+__global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
     tsm2r_stream_tma(const DynArgs<T> a, const __grid_constant__ CUtensorMap tmA) {
-  using Cfg = TmaCfg<T, NT>;
+  using Cfg = typename Consumer::Cfg;  // row-block height / stage width of this consumer
   constexpr int R = Cfg::R, KC = Cfg::KC, STAGES = Cfg::STAGES;
   extern __shared__ __align__(1024) unsigned char smem[];
   T* sA = reinterpret_cast<T*>(smem);

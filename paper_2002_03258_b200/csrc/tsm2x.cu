@@ -351,28 +351,30 @@ static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, 
   *grid = std::min<int64_t>(G_full, (it->total + it->batch - 1) / it->batch);
 }
 
-template <typename T, int NT, int KIND>
+template <typename T, int NT, int KIND, int RPT, int CW>
 struct ConsumerFor {
-  using type = FmaConsumer<T, NT>;
+  using type = FmaConsumer<T, NT, RPT, CW>;
 };
-template <int NT>
-struct ConsumerFor<double, NT, kDmma> {
-  using type = typename std::conditional<(NT == 8 || NT == 16), DmmaConsumer<(NT >= 8 ? NT : 8)>,
-                                         FmaConsumer<double, NT>>::type;
+template <int NT, int RPT, int CW>
+struct ConsumerFor<double, NT, kDmma, RPT, CW> {
+  using type = typename std::conditional<((NT == 8 || NT == 16) && RPT == 2 && CW == 8),
+                                         DmmaConsumer<(NT >= 8 ? NT : 8)>, FmaConsumer<double, NT, RPT, CW>>::type;
 };
-template <typename T, int NT>
-struct ConsumerFor<T, NT, kNull> {
-  using type = NullConsumer<T, NT>;
+template <typename T, int NT, int RPT, int CW>
+struct ConsumerFor<T, NT, kNull, RPT, CW> {
+  using type = NullConsumer<T, NT, RPT, CW>;
 };
-template <int NT>
-struct ConsumerFor<float, NT, kFfma2> {
-  using type = typename std::conditional<(NT >= 2), Ffma2Consumer<(NT >= 2 ? NT : 2)>, FmaConsumer<float, NT>>::type;
+template <int NT, int RPT, int CW>
+struct ConsumerFor<float, NT, kFfma2, RPT, CW> {
+  using type = typename std::conditional<(NT >= 2 && RPT == 4 && CW == 8), Ffma2Consumer<(NT >= 2 ? NT : 2)>,
+                                         FmaConsumer<float, NT, RPT, CW>>::type;
 };
 
-template <typename T, int NT, int KIND>
+template <typename T, int NT, int KIND, int RPT, int CW>
 static int launch_tma_kernel(const DynArgs<T>& a_in, const CUtensorMap& tmap_in, int64_t G, cudaStream_t s) {
-  using Cfg = TmaCfg<T, NT>;
-  using Cons = typename ConsumerFor<T, NT, KIND>::type;
+  using Cons = typename ConsumerFor<T, NT, KIND, RPT, CW>::type;
+  using Cfg = typename Cons::Cfg;
+  static_assert(Cfg::R == TmaCfg<T, NT, RPT, CW>::R, "consumer / plan row-block mismatch");
   auto kern = tsm2r_stream_tma<T, NT, Cons>;
   TSM2X_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   DynArgs<T> a = a_in;
@@ -393,11 +395,11 @@ static int launch_tma_kernel(const DynArgs<T>& a_in, const CUtensorMap& tmap_in,
 }
 
 // TMA flavour, dynamic items (tsm2r_tma.cuh): item sizes from the per-CTA share of the work.
-template <typename T, int NT>
+template <typename T, int NT, int RPT = Vec<T>::N, int CW = 8>
 static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k, int w, const T* A, int64_t lda,
                          const T* B, int64_t ldb, T* C, int64_t ldc, bool c_is_zero, bool ordered,
                          cudaStream_t s) {
-  using Cfg = TmaCfg<T, NT>;
+  using Cfg = TmaCfg<T, NT, RPT, CW>;
   const size_t eb = sizeof(T);
   const Tuning tu = current_tuning();
   DynArgs<T> a;
@@ -417,7 +419,8 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   a.ordered = ordered ? 1 : 0;
   const bool atomic_split = split && !a.ordered;
   const size_t acc_bytes = (atomic_split && sizeof(T) == 4) ? (size_t)a.ldacc * NT * sizeof(double) : 0;
-  const int kind = pick_consumer_rt(sizeof(T), NT, split, tu);
+  int kind = pick_consumer_rt(sizeof(T), NT, split, tu);
+  if ((RPT != Vec<T>::N || CW != 8) && (kind == kDmma || kind == kFfma2)) kind = kFma;  // default geometry only
   const size_t bt_bytes = align_up((size_t)kpad * NT * sizeof(T), 256);
   TSM2X_TRY(ws_reserve(ws, bt_bytes + acc_bytes, (size_t)it.num_rb + 8, s));
   a.tickets = reinterpret_cast<unsigned*>(ws->counters + 8);  // zero between launches
@@ -456,13 +459,13 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   const bool timed = t_ev_start && t_ev_stop;
   if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
   if (kind == kDmma)
-    TSM2X_TRY((launch_tma_kernel<T, NT, kDmma>(a, tmap, G, s)));
+    TSM2X_TRY((launch_tma_kernel<T, NT, kDmma, RPT, CW>(a, tmap, G, s)));
   else if (kind == kFfma2)
-    TSM2X_TRY((launch_tma_kernel<T, NT, kFfma2>(a, tmap, G, s)));
+    TSM2X_TRY((launch_tma_kernel<T, NT, kFfma2, RPT, CW>(a, tmap, G, s)));
   else if (kind == kNull)
-    TSM2X_TRY((launch_tma_kernel<T, NT, kNull>(a, tmap, G, s)));
+    TSM2X_TRY((launch_tma_kernel<T, NT, kNull, RPT, CW>(a, tmap, G, s)));
   else
-    TSM2X_TRY((launch_tma_kernel<T, NT, kFma>(a, tmap, G, s)));
+    TSM2X_TRY((launch_tma_kernel<T, NT, kFma, RPT, CW>(a, tmap, G, s)));
   if (timed) {
     TSM2X_CUDA(cudaEventRecord(t_ev_stop, s));
     t_ev_start = t_ev_stop = nullptr;
@@ -611,7 +614,29 @@ static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m,
   const int combine = current_tuning().combine;
   if (tma && combine == 3) return run_tsm2r_tma_static<T, NT>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, s);
   const bool ordered = combine == 1 || (combine == 0 && deterministic);
-  if (tma) return run_tsm2r_tma<T, NT>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
+  if (tma) {
+    // rows per consumer thread (row-block height R = 256 * rpt): TSM2X_RPT overrides for
+    // experiments on fp64 8-column passes (1, 2, 4, 8); the default is one 16-byte vector's worth
+    static const int env_rpt = [] {
+      const char* e = getenv("TSM2X_RPT");
+      return e ? atoi(e) : 0;
+    }();
+    static const int env_cw = [] {
+      const char* e = getenv("TSM2X_CW");
+      return e ? atoi(e) : 0;
+    }();
+    if constexpr (sizeof(T) == 8 && NT == 8) {
+      if (env_cw == 16) return run_tsm2r_tma<T, NT, 2, 16>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
+      if (env_cw == 12) return run_tsm2r_tma<T, NT, 2, 12>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
+      switch (env_rpt) {
+        case 1: return run_tsm2r_tma<T, NT, 1>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
+        case 4: return run_tsm2r_tma<T, NT, 4>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
+        case 8: return run_tsm2r_tma<T, NT, 8>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
+        default: break;
+      }
+    }
+    return run_tsm2r_tma<T, NT>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
+  }
   return run_tsm2r_ldg<T, NT>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, s);
 }
 

@@ -75,6 +75,9 @@ def sustain_main():
     h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
     cfgs = [("r8", 30720, 30720, 8, torch.float64), ("r2", 30720, 30720, 2, torch.float64),
             ("r16", 30720, 30720, 16, torch.float64), ("f16", 32768, 32768, 16, torch.float32)]
+    only = os.environ.get("QB_CONFIGS")
+    if only:
+        cfgs = [c for c in cfgs if c[0] in only.split(",")]
     for name, m, k, n, dt in cfgs:
         A = tsm.colmajor_empty(m, k, dt, "cuda")
         tsm.fill_uniform(A, 1)
@@ -82,7 +85,7 @@ def sustain_main():
         tsm.fill_uniform(B, 2)
         C = tsm.colmajor_empty(m, n, dt, "cuda")
         C.zero_()
-        for det in (False, True):
+        for det in ((False,) if os.environ.get("QB_NO_DET") else (False, True)):
             samples = []
             stop = threading.Event()
 
