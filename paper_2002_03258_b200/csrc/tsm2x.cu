@@ -307,7 +307,7 @@ static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
   if (want == kFma) return kFma;
   if (want == kDmma) return dmma_ok ? kDmma : kFma;
   if (want == kFfma2) return ffma2_ok ? kFfma2 : kFma;
-  if (dmma_ok && split && nt == 16) return kDmma;  // n=8: DFMA sustains higher clocks (profiles/abtest_r01.json)
+  if (dmma_ok && nt == 16) return kDmma;  // n=8: DFMA sustains higher clocks (profiles/abtest_r01*.json)
   if (ffma2_ok) return kFfma2;
   return kFma;
 }
@@ -327,7 +327,7 @@ static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, 
       tu.big_kb > 0 ? std::max(small_b, tu.big_kb * 1024.0) : std::min(4.0 * 1024 * 1024, std::max(small_b, per_cta / 6));
   const int64_t ksmall = std::max<int64_t>(KC, (int64_t)align_up((size_t)(small_b / col_bytes), KC));
   const int64_t kbig = std::max<int64_t>(ksmall, (int64_t)align_up((size_t)(big_b / col_bytes), KC));
-  const double batch_b = tu.batch_kb > 0 ? tu.batch_kb * 1024.0 : 1024.0 * 1024;
+  const double batch_b = tu.batch_kb > 0 ? tu.batch_kb * 1024.0 : 256.0 * 1024;  // abtest_r01d.json
   if ((double)k * col_bytes <= 1024.0 * 1024 || k <= ksmall) {
     // single-chunk row blocks (TSM2L shapes): no split, batched dispatch
     it->nbig = 0;

@@ -18,8 +18,9 @@ def test_plan_config2_tsm2r():
 
 def test_plan_tsm2l_single_chunk():
     p = tuning.plan("double", 1 << 24, 16, 16)
-    assert p["impl"] == "tma" and p["consumer"] == "fma"
+    assert p["impl"] == "tma" and p["consumer"] == "dmma"  # fp64 16-column passes (abtest_r01e.json)
     assert p["nbig"] == 0 and p["nsmall"] == 1 and p["batch"] > 1
+    assert tuning.plan("double", 1 << 24, 16, 8)["consumer"] == "fma"
 
 
 def test_plan_fp32_and_wide():
