@@ -100,6 +100,15 @@ int tsm2x_run_host(int variant, int precision, int64_t m, int64_t k, int64_t n,
                    const void* C_in, void* C_out, int64_t ldc,
                    const tsm2x_params* params, uint32_t flags, int device);
 
+/* tsm2x_run_host over several GPUs of one process: rows of A / C are split into contiguous
+ * 32-row-aligned shards, one per entry of devices[] (a device may repeat), each shard runs the
+ * host pipeline on its own thread, so the PCIe links (the end-to-end bound) add up. B is copied to
+ * every device; rows are independent (reference SPEC.md:262), so no reduction. Synchronous. */
+int tsm2x_run_host_multi(int variant, int precision, int64_t m, int64_t k, int64_t n,
+                         const void* A, int64_t lda, const void* B, int64_t ldb,
+                         const void* C_in, void* C_out, int64_t ldc,
+                         const tsm2x_params* params, uint32_t flags, int ndev, const int* devices);
+
 /* Synthetic-input utility (not a reference interface): fills the rows x cols column-major
  * block at ptr (leading dimension ld) with the counter-based uniform [0, 1) generator
  *   x = splitmix64(seed * 0x9E3779B97F4A7C15 + ((col_offset + j) << 32 | (row_offset + i)))

@@ -12,7 +12,7 @@ from .core import (  # noqa: F401
     Variant,
     validate_problem,
 )
-from .kernels import colmajor_empty, fill_uniform, gemm, run_native, simulate  # noqa: F401
+from .kernels import colmajor_empty, fill_uniform, gemm, run_native, run_native_multi, simulate  # noqa: F401
 
 __all__ = [
     "KernelParams",
@@ -24,6 +24,7 @@ __all__ = [
     "fill_uniform",
     "gemm",
     "run_native",
+    "run_native_multi",
     "simulate",
     "validate_problem",
 ]

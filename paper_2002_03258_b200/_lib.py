@@ -23,6 +23,7 @@ EXPORTS = (
     "tsm2x_run",
     "tsm2x_run_ex",
     "tsm2x_run_host",
+    "tsm2x_run_host_multi",
     "tsm2x_fill_uniform",
     "tsm2x_last_error",
     "tsm2x_version",
@@ -81,12 +82,15 @@ def load() -> ctypes.CDLL:
         lib.tsm2x_run.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, pp, u32, vp]
         lib.tsm2x_run_ex.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, pp, u32, i32, vp]
         lib.tsm2x_run_host.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, vp, i64, pp, u32, i32]
+        lib.tsm2x_run_host_multi.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, vp, i64, pp, u32, i32,
+                                             ctypes.POINTER(ctypes.c_int)]
         lib.tsm2x_fill_uniform.argtypes = [i32, i64, i64, vp, i64, i64, i64, ctypes.c_uint64, vp]
         lib.tsm2x_set_kernel_events.argtypes = [vp, vp]
         lib.tsm2x_set_tuning.argtypes = [ctypes.POINTER(Tuning)]
         lib.tsm2x_get_tuning.argtypes = [ctypes.POINTER(Tuning)]
         lib.tsm2x_plan_for.argtypes = [i32, i64, i64, i64, i64, i32, u32, i32, ctypes.POINTER(Plan)]
-        for name in ("tsm2x_validate", "tsm2x_run", "tsm2x_run_ex", "tsm2x_run_host", "tsm2x_fill_uniform",
+        for name in ("tsm2x_validate", "tsm2x_run", "tsm2x_run_ex", "tsm2x_run_host", "tsm2x_run_host_multi",
+                     "tsm2x_fill_uniform",
                      "tsm2x_version", "tsm2x_set_kernel_events", "tsm2x_set_tuning", "tsm2x_get_tuning",
                      "tsm2x_plan_for"):
             getattr(lib, name).restype = ctypes.c_int

@@ -1125,6 +1125,37 @@ int tsm2x_run_host(int variant, int precision, int64_t m, int64_t k, int64_t n, 
                            (float*)C_out, ldc, params, flags, device);
 }
 
+int tsm2x_run_host_multi(int variant, int precision, int64_t m, int64_t k, int64_t n, const void* A, int64_t lda,
+                         const void* B, int64_t ldb, const void* C_in, void* C_out, int64_t ldc,
+                         const tsm2x_params* params, uint32_t flags, int ndev, const int* devices) {
+  TSM2X_TRY(validate(variant, precision, m, k, n, params));
+  if (ndev < 1 || !devices) return fail(TSM2X_EINVAL, "need at least one device");
+  if (!A || !B || !C_out || (!C_in && !(flags & TSM2X_FLAG_C_IS_ZERO))) return fail(TSM2X_EINVAL, "null host pointer");
+  const size_t eb = precision == TSM2X_DOUBLE ? 8 : 4;
+  // contiguous row shards in 32-row units (paper_2002_03258_b200.multi.row_partition)
+  const int64_t blocks = (m + 31) / 32;
+  std::vector<int> rc(ndev, TSM2X_OK);
+  std::vector<std::string> msg(ndev);
+  std::vector<std::thread> th;
+  for (int d = 0; d < ndev; ++d) {
+    const int64_t r0 = std::min<int64_t>(m, blocks * d / ndev * 32);
+    const int64_t r1 = std::min<int64_t>(m, blocks * (d + 1) / ndev * 32);
+    if (r1 <= r0) continue;
+    th.emplace_back([=, &rc, &msg] {
+      const char* a = static_cast<const char*>(A) + r0 * eb;
+      const char* ci = C_in ? static_cast<const char*>(C_in) + r0 * eb : nullptr;
+      char* co = static_cast<char*>(C_out) + r0 * eb;
+      rc[d] = tsm2x_run_host(variant, precision, r1 - r0, k, n, a, lda, B, ldb, ci, co, ldc, params, flags,
+                             devices[d]);
+      if (rc[d] != TSM2X_OK) msg[d] = t_err;
+    });
+  }
+  for (auto& x : th) x.join();
+  for (int d = 0; d < ndev; ++d)
+    if (rc[d] != TSM2X_OK) return fail(rc[d], "device %d: %s", devices[d], msg[d].c_str());
+  return TSM2X_OK;
+}
+
 int tsm2x_fill_uniform(int precision, int64_t rows, int64_t cols, void* ptr, int64_t ld, int64_t row_offset,
                        int64_t col_offset, uint64_t seed, void* stream) {
   if (rows < 1 || cols < 1 || ld < rows || !ptr || row_offset < 0 || col_offset < 0 ||

@@ -61,6 +61,34 @@ def run_native(variant, A, B, C, params) -> Matrix:
     return Matrix._adopt(m, n, out, prec)
 
 
+def run_native_multi(variant, A, B, C, params, devices) -> Matrix:
+    """run_native over several GPUs of this process (``tsm2x_run_host_multi``): contiguous
+    32-row-aligned row shards, one per entry of ``devices`` (may repeat), each streamed by its
+    own host thread, so the per-GPU PCIe links add up. Same result contract as run_native."""
+    variant = Variant.coerce(variant)
+    m, k, n = check_dims(A, B, C)
+    validate_params_for(params, m, k, n)
+    prec = Precision.coerce(A.precision)
+    dtype = prec.dtype
+    a, b, c = _flat(A, dtype), _flat(B, dtype), _flat(C, dtype)
+    flags = 0
+    if variant is Variant.L_OPT2:
+        if np.any(c != 0):
+            raise ValueError("L_OPT2 stores partial sums to C and requires a zeroed C")
+        flags |= _lib.FLAG_C_IS_ZERO
+    devices = list(devices)
+    if not devices:
+        raise ValueError("devices must not be empty")
+    devs = (ctypes.c_int * len(devices))(*devices)
+    out = np.empty(m * n, dtype=dtype)
+    p = _params_struct(params)
+    rc = _lib.load().tsm2x_run_host_multi(
+        variant.ordinal, _lib.DOUBLE if prec is Precision.DOUBLE else _lib.SINGLE, m, k, n, a.ctypes.data, m,
+        b.ctypes.data, k, c.ctypes.data, out.ctypes.data, m, ctypes.byref(p), flags, len(devices), devs)
+    _lib.check(rc)
+    return Matrix._adopt(m, n, out, prec)
+
+
 def simulate(*args, **kwargs):
     raise NotImplementedError(
         "simulate() is the reference's CPU SIMT model (kernels.py:371-388); on B200 the real kernels run "

@@ -419,3 +419,15 @@ print("ok")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0]])
+def test_run_native_multi_device_shards(devices):
+    """tsm2x_run_host_multi: row shards on (repeated) devices, TSM2R and TSM2L, nonzero C."""
+    tsm = _tsm()
+    rng = np.random.default_rng(len(devices))
+    for (m, k, n) in [(4099, 3000, 8), (70001, 16, 16), (33, 100, 3)]:
+        A, B, C0 = rng.random((m, k)), rng.random((k, n)), rng.random((m, n))
+        out = tsm.run_native_multi(tsm.Variant.V3, tsm.Matrix.from_2d(A, "double"), tsm.Matrix.from_2d(B, "double"),
+                                   tsm.Matrix.from_2d(C0, "double"), tsm.KernelParams(t2=min(4, n)), devices)
+        _check(out.to_2d(), naive_gemm(A, B, C0), k, "double", what=(devices, m, k, n))
