@@ -25,8 +25,6 @@
 #pragma once
 #include <cuda.h>
 
-#include <new>
-
 #include "common.cuh"
 #include "tsm2r_stream.cuh"
 
@@ -138,23 +136,19 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // Ordered combine of split row blocks: chunk c of row block rb may update C only after chunks
 // 0..c-1 did (ticket == c), so C's rows receive their partial sums in column order whatever
 // CTA ran which item — bitwise reproducible. Column-chunk-major dispatch hands chunk c of a row
-// block out ~one round of items before chunk c+1, so the wait is almost never taken, and the
-// consumers' pause is absorbed by the TMA ring (the producer keeps streaming).
-struct TicketGuard {
-  const unsigned* t;
-  unsigned c;
-  bool leader;
-  __device__ __forceinline__ TicketGuard(const unsigned* tick, unsigned chunk, bool lead)
-      : t(tick), c(chunk), leader(lead) {
-    if (leader)
-      while (ld_acquire(t) != c) __nanosleep(128);
-    ConsumerSync()();
-  }
-  __device__ __forceinline__ void release(unsigned* tick, unsigned next) const {
-    ConsumerSync()();
-    if (leader) st_release(tick, next);
-  }
-};
+// block out ~one round of items before chunk c+1, so the wait is rarely long; the pause costs
+// 2-30 % (profiles/abtest_r01b.json), which is why it is opt-in (deterministic=True).
+// Called by all consumer threads; the leader spins, the named barrier publishes its acquire.
+__device__ __forceinline__ void ticket_wait(const unsigned* tick, unsigned chunk, bool leader) {
+  if (leader)
+    while (ld_acquire(tick) != chunk) __nanosleep(128);
+  ConsumerSync()();
+}
+// All consumers' C stores precede the barrier; the leader's release store hands the row block on.
+__device__ __forceinline__ void ticket_pass(unsigned* tick, unsigned next, bool leader) {
+  ConsumerSync()();
+  if (leader) st_release(tick, next);
+}
 
 // Epilogue of one item. Consumer thread ct owns rows ct + 256*r (r < RPT) of the row block, so
 // every warp-wide access below touches 32 consecutive elements of a C column: coalesced stores
@@ -167,9 +161,7 @@ __device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int
   const int64_t nch = a.it.nch();
   const int64_t c = nch == 1 ? 0 : a.it.chunk(item);
   if (nch == 1 || a.ordered) {
-    TicketGuard* g = nullptr;
-    alignas(TicketGuard) unsigned char gbuf[sizeof(TicketGuard)];
-    if (nch > 1) g = new (gbuf) TicketGuard(a.tickets + rb, (unsigned)c, ct == 0);
+    if (nch > 1) ticket_wait(a.tickets + rb, (unsigned)c, ct == 0);
     // all loads of C first (one round trip, not NT*RPT dependent ones), then the stores; the
     // first chunk starts from C's input (or from zero under the zero-C contract)
     const bool read_c = c > 0 || !a.c_is_zero;
@@ -196,7 +188,7 @@ __device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int
         }
       }
     }
-    if (g) g->release(a.tickets + rb, c + 1 == nch ? 0u : (unsigned)(c + 1));
+    if (nch > 1) ticket_pass(a.tickets + rb, c + 1 == nch ? 0u : (unsigned)(c + 1), ct == 0);
     return;
   }
 #pragma unroll
@@ -395,9 +387,8 @@ struct DmmaConsumer {
         }
       return;
     }
-    TicketGuard* gd = nullptr;
-    alignas(TicketGuard) unsigned char gbuf[sizeof(TicketGuard)];
-    if (nch > 1) gd = new (gbuf) TicketGuard(a.tickets + rb, (unsigned)c, warp == 0 && lane == 0);
+    const bool leader = warp == 0 && lane == 0;
+    if (nch > 1) ticket_wait(a.tickets + rb, (unsigned)c, leader);
     const bool read_c = c > 0 || !a.c_is_zero;
     double old[4][2][NTI][2];
 #pragma unroll
@@ -426,7 +417,7 @@ struct DmmaConsumer {
             if (j < a.w) __stcg(a.C + j * a.ldc + row, old[q][mt][nt][e] + acc[q][mt][nt][e]);
           }
       }
-    if (gd) gd->release(a.tickets + rb, c + 1 == nch ? 0u : (unsigned)(c + 1));
+    if (nch > 1) ticket_pass(a.tickets + rb, c + 1 == nch ? 0u : (unsigned)(c + 1), leader);
   }
 };
 
