@@ -320,13 +320,16 @@ struct Ffma2Consumer {
 // so each B fragment is one LDS.64 per lane. 32 DMMAs per warp per stage replace 256 DFMAs and
 // 64 LDS.128 of the FMA consumer; the FP64 datapath is shared (measured), so this buys issue
 // slots and power, not peak.
-template <int NT>
+template <int NT, int CW_ = 8>
 struct DmmaConsumer {
-  using Cfg = TmaCfg<double, NT>;
+  using Cfg = TmaCfg<double, NT, 16 / CW_, CW_>;  // R = 512 rows for CW_ in {8, 16}
   static constexpr bool kFragB = true;
   static_assert(NT == 8 || NT == 16, "DMMA consumer needs NT in {8, 16}");
-  static constexpr int NTI = NT / 8;  // N tiles
-  double acc[4][2][NTI][2];           // [row group][M tile (even/odd rows)][N tile][2 columns]
+  static_assert(CW_ == 8 || CW_ == 16, "DMMA consumer: 8 or 16 consumer warps");
+  static constexpr int NTI = NT / 8;       // N tiles
+  static constexpr int RW = Cfg::R / CW_;  // rows per warp (64 or 32)
+  static constexpr int Q = RW / 16;        // 16-row groups per warp
+  double acc[Q][2][NTI][2];                // [row group][M tile (even/odd rows)][N tile][2 columns]
   int warp, lane;
   __device__ __forceinline__ void init(int consumer_thread) {
     warp = consumer_thread / 32;
@@ -335,44 +338,60 @@ struct DmmaConsumer {
   }
   __device__ __forceinline__ void zero() {
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < Q; ++q)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt) acc[q][mt][nt][0] = acc[q][mt][nt][1] = 0.0;
   }
-  __device__ __forceinline__ void stage(const double* sA, const double* sB) {
+  // One stage's fragments, loaded from shared memory in one go before its DMMAs. (A look-ahead
+  // variant that loaded stage s+1 before issuing stage s's DMMAs was slower under the power cap —
+  // 1.32 vs 1.21 ms at n=8, profiles/README.md — the consumer is not LDS-latency bound.)
+  static constexpr int KS = Cfg::KC / 4;  // k-steps of 4 columns per stage
+  struct Frag {
+    double b[KS][NTI];
+    double2 av[KS][Q];
+  };
+  __device__ __forceinline__ void load(const double* sA, const double* sB, Frag& f) const {
     const int g = lane >> 2, t = lane & 3;
-    // box = warp / 4, rows within the box start at 64 * (warp % 4)
-    const double* As = sA + (warp >> 2) * (Cfg::BOX * Cfg::KC) + (64 * (warp & 3) + 2 * g);
+    // the warp's rows start at RW * warp: TMA box (RW * warp) / 256, offset (RW * warp) % 256
+    const double* As = sA + (RW * warp / Cfg::BOX) * (Cfg::BOX * Cfg::KC) + (RW * warp % Cfg::BOX + 2 * g);
 #pragma unroll
-    for (int ks = 0; ks < Cfg::KC / 4; ++ks) {
-      double b[NTI];
+    for (int ks = 0; ks < KS; ++ks) {
 #pragma unroll
-      for (int nt = 0; nt < NTI; ++nt) b[nt] = sB[(ks * NTI + nt) * 32 + lane];
+      for (int nt = 0; nt < NTI; ++nt) f.b[ks][nt] = sB[(ks * NTI + nt) * 32 + lane];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double2 av = *reinterpret_cast<const double2*>(As + (4 * ks + t) * Cfg::BOX + 16 * q);
+      for (int q = 0; q < Q; ++q) f.av[ks][q] = *reinterpret_cast<const double2*>(As + (4 * ks + t) * Cfg::BOX + 16 * q);
+    }
+  }
+  __device__ __forceinline__ void mma(const Frag& f) {
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt) {
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                       : "+d"(acc[q][0][nt][0]), "+d"(acc[q][0][nt][1]) : "d"(av.x), "d"(b[nt]));
+                       : "+d"(acc[q][0][nt][0]), "+d"(acc[q][0][nt][1]) : "d"(f.av[ks][q].x), "d"(f.b[ks][nt]));
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                       : "+d"(acc[q][1][nt][0]), "+d"(acc[q][1][nt][1]) : "d"(av.y), "d"(b[nt]));
+                       : "+d"(acc[q][1][nt][0]), "+d"(acc[q][1][nt][1]) : "d"(f.av[ks][q].y), "d"(f.b[ks][nt]));
         }
-      }
-    }
   }
-  // accumulator (q, mt, nt, e) holds row 64w + 16q + 2g + mt, column 8nt + 2t + e
+  __device__ __forceinline__ void stage(const double* sA, const double* sB) {
+    Frag f;
+    load(sA, sB, f);
+    mma(f);
+  }
+  // accumulator (q, mt, nt, e) holds row RW*w + 16q + 2g + mt, column 8nt + 2t + e
   __device__ __forceinline__ void finish(const DynArgs<double>& a, int64_t rb, int64_t item) const {
     const int g = lane >> 2, t = lane & 3;
-    const int64_t base = rb * Cfg::R + 64 * warp + 2 * g;
+    const int64_t base = rb * Cfg::R + RW * warp + 2 * g;
     const int64_t nch = a.it.nch();
     const int64_t c = nch == 1 ? 0 : a.it.chunk(item);
     const bool rmw = nch == 1 || a.ordered;
     if (!rmw) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < Q; ++q)
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
           const int64_t row = base + 16 * q + mt;
@@ -390,9 +409,43 @@ struct DmmaConsumer {
     const bool leader = warp == 0 && lane == 0;
     if (nch > 1) ticket_wait(a.tickets + rb, (unsigned)c, leader);
     const bool read_c = c > 0 || !a.c_is_zero;
-    double old[4][2][NTI][2];
+    if (a.vec_c && rb * Cfg::R + Cfg::R <= a.m) {
+      // whole row block, 16-B aligned C: the lane's two rows (2g, 2g+1) of a column are adjacent,
+      // so each access is one 16-byte vector and a warp instruction covers four full 128-B lines
+      // (8 row pairs x 4 columns) instead of eight half-filled sectors per column
+      double2 old[Q][NTI][2];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = 8 * nt + 2 * t + e;
+            old[q][nt][e] = (read_c && j < a.w)
+                                ? __ldcg(reinterpret_cast<const double2*>(a.C + j * a.ldc + base + 16 * q))
+                                : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = 8 * nt + 2 * t + e;
+            if (j >= a.w) continue;
+            const double2 v = make_double2(old[q][nt][e].x + acc[q][0][nt][e], old[q][nt][e].y + acc[q][1][nt][e]);
+            double2* dst = reinterpret_cast<double2*>(a.C + j * a.ldc + base + 16 * q);
+            if (nch == 1)
+              __stcs(dst, v);
+            else
+              __stcg(dst, v);
+          }
+      if (nch > 1) ticket_pass(a.tickets + rb, c + 1 == nch ? 0u : (unsigned)(c + 1), leader);
+      return;
+    }
+    double old[Q][2][NTI][2];
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -404,7 +457,7 @@ struct DmmaConsumer {
             old[q][mt][nt][e] = (read_c && row < a.m && j < a.w) ? __ldcg(a.C + j * a.ldc + row) : 0.0;
           }
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < Q; ++q)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         const int64_t row = base + 16 * q + mt;

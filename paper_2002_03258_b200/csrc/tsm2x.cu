@@ -285,8 +285,8 @@ static Tuning current_tuning() {
   return g_tune;
 }
 
-// Consumer choice (tsm2r_tma.cuh): DMMA for fp64 split row blocks at NT >= 8 (issue slots /
-// power at the FP64-heavy widths), packed FFMA2 for fp32 at NT >= 2, plain FMA otherwise.
+// Consumer choice (tsm2r_tma.cuh): DMMA for fp64 passes of width 8 or 16 (fewer issue slots and
+// less energy per FMA than DFMA), packed FFMA2 for fp32 at NT >= 2, plain FMA otherwise.
 // TSM2X_CONSUMER=fma|dmma|ffma2 in the environment overrides (ablation runs).
 enum ConsumerKind { kFma = 0, kDmma = 1, kFfma2 = 2, kNull = 3 };
 
@@ -301,13 +301,20 @@ static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
     return -1;
   }();
   if (env == kNull) return kNull;
-  const int want = env >= 0 ? env : (tu.consumer == 1 ? kFma : tu.consumer == 2 ? kDmma : tu.consumer == 3 ? kFfma2 : -1);
+  const int want = env >= 0 ? env
+                            : (tu.consumer == 1   ? kFma
+                               : tu.consumer == 2 ? kDmma
+                               : tu.consumer == 3 ? kFfma2
+                                                  : -1);
   const bool dmma_ok = eb == 8 && (nt == 8 || nt == 16);
   const bool ffma2_ok = eb == 4 && nt >= 2;
   if (want == kFma) return kFma;
   if (want == kDmma) return dmma_ok ? kDmma : kFma;
   if (want == kFfma2) return ffma2_ok ? kFfma2 : kFma;
-  if (dmma_ok && nt == 16) return kDmma;  // n=8: DFMA sustains higher clocks (profiles/abtest_r01*.json)
+  // fp64 8- and 16-column passes: DMMA. At n=8 DMMA and DFMA take the same time under the 1000 W
+  // cap on most parts (DMMA runs ~300 MHz higher for the same energy) and DMMA is up to 3 %
+  // faster on others (profiles/envab_r01.json); at n=16 DMMA wins outright
+  if (dmma_ok) return kDmma;
   if (ffma2_ok) return kFfma2;
   return kFma;
 }
@@ -357,8 +364,9 @@ struct ConsumerFor {
 };
 template <int NT, int RPT, int CW>
 struct ConsumerFor<double, NT, kDmma, RPT, CW> {
-  using type = typename std::conditional<((NT == 8 || NT == 16) && RPT == 2 && CW == 8),
-                                         DmmaConsumer<(NT >= 8 ? NT : 8)>, FmaConsumer<double, NT, RPT, CW>>::type;
+  using type = typename std::conditional<((NT == 8 || NT == 16) && RPT * CW == 16 && (CW == 8 || CW == 16)),
+                                         DmmaConsumer<(NT >= 8 ? NT : 8), (CW == 16 ? 16 : 8)>,
+                                         FmaConsumer<double, NT, RPT, CW>>::type;
 };
 template <typename T, int NT, int RPT, int CW>
 struct ConsumerFor<T, NT, kNull, RPT, CW> {
@@ -420,7 +428,9 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   const bool atomic_split = split && !a.ordered;
   const size_t acc_bytes = (atomic_split && sizeof(T) == 4) ? (size_t)a.ldacc * NT * sizeof(double) : 0;
   int kind = pick_consumer_rt(sizeof(T), NT, split, tu);
-  if ((RPT != Vec<T>::N || CW != 8) && (kind == kDmma || kind == kFfma2)) kind = kFma;  // default geometry only
+  // DMMA: the 512-row geometries (8 warps x 2 rows or 16 warps x 1 row); FFMA2: the default one
+  if (kind == kDmma && !(RPT * CW == 16 && (CW == 8 || CW == 16))) kind = kFma;
+  if (kind == kFfma2 && (RPT != Vec<T>::N || CW != 8)) kind = kFma;
   const size_t bt_bytes = align_up((size_t)kpad * NT * sizeof(T), 256);
   TSM2X_TRY(ws_reserve(ws, bt_bytes + acc_bytes, (size_t)it.num_rb + 8, s));
   a.tickets = reinterpret_cast<unsigned*>(ws->counters + 8);  // zero between launches
@@ -625,6 +635,10 @@ static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m,
       const char* e = getenv("TSM2X_CW");
       return e ? atoi(e) : 0;
     }();
+    if constexpr (sizeof(T) == 8 && (NT == 8 || NT == 16)) {
+      if (env_cw == 16 && env_rpt == 1)  // 16 consumer warps x 1 row: 512-row blocks (DMMA-capable)
+        return run_tsm2r_tma<T, NT, 1, 16>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
+    }
     if constexpr (sizeof(T) == 8 && NT == 8) {
       if (env_cw == 16) return run_tsm2r_tma<T, NT, 2, 16>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
       if (env_cw == 12) return run_tsm2r_tma<T, NT, 2, 12>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);

@@ -40,8 +40,8 @@ IMPLS = {v: k for k, v in _lib.IMPL.items()}
 # The library's built-in defaults (tsm2x.cu make_items / pick_consumer_rt), stated here for
 # reporting; 0 in a Tuning means "use these".
 B200_DEFAULTS = {
-    "consumer": "auto: DMMA for fp64 split row blocks with 16-column passes; FFMA2 for fp32 n >= 2; else FMA "
-                "(DFMA beats DMMA at n=8 under the power cap: profiles/abtest_r01.json)",
+    "consumer": "auto: DMMA for fp64 8- and 16-column passes; FFMA2 for fp32 n >= 2; else FMA "
+                "(sustained A/B under the 1000 W cap: profiles/envab_r01.json)",
     "small_kb": "min(512 (1024 for 16-column passes), max(64, per-CTA share / 48))",
     "big_kb": "min(4096, max(small, per-CTA share / 6))",
     "tail_pct": "20 (10 for 16-column passes)",

@@ -391,9 +391,10 @@ def test_config4_fp32_sampled():
         _check(Ch[r0:r0 + 128], ref, k, "single", what=r0)
 
 
-@pytest.mark.parametrize("consumer", ["fma", "dmma", "ffma2"])
+@pytest.mark.parametrize("consumer", ["fma", "dmma", "ffma2", "dmma/cw16", "fma/cw16"])
 def test_consumer_policies_subprocess(consumer):
-    """Each TMA consumer policy (TSM2X_CONSUMER override) on split and single-chunk shapes."""
+    """Each TMA consumer policy (TSM2X_CONSUMER override; "/cw16" = the 16-consumer-warp x 1-row
+    geometry, TSM2X_CW=16 TSM2X_RPT=1) on split and single-chunk shapes."""
     import os
     import subprocess
     import sys
@@ -403,7 +404,8 @@ sys.path.insert(0, ".")
 import paper_2002_03258_b200 as tsm
 from oracle import naive_gemm, rel_frobenius
 rng = np.random.default_rng(5)
-for (m, k, n) in [(2000, 5000, 16), (1500, 3001, 8), (777, 10000, 12), (4096, 16, 16), (513, 20000, 3)]:
+for (m, k, n) in [(2000, 5000, 16), (1500, 3001, 8), (777, 10000, 12), (4096, 16, 16), (513, 20000, 3),
+                  (70001, 16, 16), (5000, 24, 8)]:
     for dt in (torch.float64, torch.float32):
         A = tsm.colmajor_empty(m, k, dt, "cuda"); A.copy_(torch.from_numpy(rng.random((m, k))).to(dt))
         B = tsm.colmajor_empty(k, n, dt, "cuda"); B.copy_(torch.from_numpy(rng.random((k, n))).to(dt))
@@ -415,7 +417,9 @@ for (m, k, n) in [(2000, 5000, 16), (1500, 3001, 8), (777, 10000, 12), (4096, 16
         assert err <= tol, (m, k, n, dt, err)
 print("ok")
 '''
-    env = dict(os.environ, TSM2X_CONSUMER=consumer)
+    env = dict(os.environ, TSM2X_CONSUMER=consumer.split("/")[0])
+    if consumer.endswith("/cw16"):
+        env.update(TSM2X_CW="16", TSM2X_RPT="1")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
