@@ -103,6 +103,8 @@ struct DynArgs {
   unsigned* tickets;  // [num_rb] next chunk allowed to update the row block; zero between launches
   Items it;
   unsigned long long* queue;  // [0] next item, [1] low 32 bits: producers finished
+  int diag = 0;                       // tsm2r_stream_tc32 diagnostics (TSM2X_TC_DIAG): skip bits
+  unsigned long long* dbg = nullptr;  // tsm2r_stream_tc32 diagnostics: cycle counters (or null)
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
@@ -344,43 +346,31 @@ struct DmmaConsumer {
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt) acc[q][mt][nt][0] = acc[q][mt][nt][1] = 0.0;
   }
-  // One stage's fragments, loaded from shared memory in one go before its DMMAs. (A look-ahead
-  // variant that loaded stage s+1 before issuing stage s's DMMAs was slower under the power cap —
-  // 1.32 vs 1.21 ms at n=8, profiles/README.md — the consumer is not LDS-latency bound.)
-  static constexpr int KS = Cfg::KC / 4;  // k-steps of 4 columns per stage
-  struct Frag {
-    double b[KS][NTI];
-    double2 av[KS][Q];
-  };
-  __device__ __forceinline__ void load(const double* sA, const double* sB, Frag& f) const {
+  // Per k-step of 4 columns: the B fragments (one LDS.64 per N tile), then per 16-row group one
+  // LDS.128 (rows 2g, 2g+1 of column t) feeding the even- and odd-row M tiles. (A variant that
+  // loaded a whole stage's fragments first — and a look-ahead loop loading stage s+1 before stage
+  // s's DMMAs — spilled at n=16 and was slower under the power cap: profiles/envab_r01.json.)
+  __device__ __forceinline__ void stage(const double* sA, const double* sB) {
     const int g = lane >> 2, t = lane & 3;
     // the warp's rows start at RW * warp: TMA box (RW * warp) / 256, offset (RW * warp) % 256
     const double* As = sA + (RW * warp / Cfg::BOX) * (Cfg::BOX * Cfg::KC) + (RW * warp % Cfg::BOX + 2 * g);
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
+    for (int ks = 0; ks < Cfg::KC / 4; ++ks) {
+      double b[NTI];
 #pragma unroll
-      for (int nt = 0; nt < NTI; ++nt) f.b[ks][nt] = sB[(ks * NTI + nt) * 32 + lane];
+      for (int nt = 0; nt < NTI; ++nt) b[nt] = sB[(ks * NTI + nt) * 32 + lane];
 #pragma unroll
-      for (int q = 0; q < Q; ++q) f.av[ks][q] = *reinterpret_cast<const double2*>(As + (4 * ks + t) * Cfg::BOX + 16 * q);
-    }
-  }
-  __device__ __forceinline__ void mma(const Frag& f) {
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-      for (int q = 0; q < Q; ++q)
+      for (int q = 0; q < Q; ++q) {
+        const double2 av = *reinterpret_cast<const double2*>(As + (4 * ks + t) * Cfg::BOX + 16 * q);
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt) {
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                       : "+d"(acc[q][0][nt][0]), "+d"(acc[q][0][nt][1]) : "d"(f.av[ks][q].x), "d"(f.b[ks][nt]));
+                       : "+d"(acc[q][0][nt][0]), "+d"(acc[q][0][nt][1]) : "d"(av.x), "d"(b[nt]));
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                       : "+d"(acc[q][1][nt][0]), "+d"(acc[q][1][nt][1]) : "d"(f.av[ks][q].y), "d"(f.b[ks][nt]));
+                       : "+d"(acc[q][1][nt][0]), "+d"(acc[q][1][nt][1]) : "d"(av.y), "d"(b[nt]));
         }
-  }
-  __device__ __forceinline__ void stage(const double* sA, const double* sB) {
-    Frag f;
-    load(sA, sB, f);
-    mma(f);
+      }
+    }
   }
   // accumulator (q, mt, nt, e) holds row RW*w + 16q + 2g + mt, column 8nt + 2t + e
   __device__ __forceinline__ void finish(const DynArgs<double>& a, int64_t rb, int64_t item) const {

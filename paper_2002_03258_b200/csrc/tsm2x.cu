@@ -24,6 +24,7 @@
 #include "tsm2r_stream.cuh"
 #include "tsm2r_tma.cuh"
 #include "tsm2r_tma_static.cuh"
+#include "tsm2r_tc32.cuh"
 
 namespace tsm2x {
 
@@ -210,6 +211,32 @@ static int encode_a_map(CUtensorMap* map, const void* A, int64_t m, int64_t k, i
   return TSM2X_OK;
 }
 
+// A as a 3-D tensor {32 rows, k columns, ceil(m/32) row chunks} for tsm2r_stream_tc32: a box
+// {32, 16, 16} lands in smem as [chunk][column][32 rows] with the 128B / 32B-atom swizzle — the
+// UMMA SWIZZLE_128B_BASE32B MN-major layout. Needs lda >= roundup(m, 32) (the last chunk's rows
+// past m are read, never stored).
+static int encode_a_map_tc32(CUtensorMap* map, const float* A, int64_t m, int64_t k, int64_t lda) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!encode) return fail(TSM2X_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  cuuint64_t dims[3] = {32, (cuuint64_t)k, (cuuint64_t)((m + 31) / 32)};
+  cuuint64_t strides[2] = {(cuuint64_t)(lda * 4), 128};
+  cuuint32_t box[3] = {32, (cuuint32_t)Tc32Cfg::KC, (cuuint32_t)(Tc32Cfg::R / 32)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(A), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TSM2X_ECUDA, "cuTensorMapEncodeTiled (tc32) failed (%d)", (int)r);
+  return TSM2X_OK;
+}
+
 // ---- paper ablation kernels (V0/V1/V2), launched with the caller's t1/t2/t3 -----------------
 template <typename T, int NT>
 static int launch_ablation_nt(int variant, int64_t m, int64_t k, int64_t n, const T* A, int64_t lda, const T* B,
@@ -285,10 +312,11 @@ static Tuning current_tuning() {
   return g_tune;
 }
 
-// Consumer choice (tsm2r_tma.cuh): DMMA for fp64 passes of width 8 or 16 (fewer issue slots and
-// less energy per FMA than DFMA), packed FFMA2 for fp32 at NT >= 2, plain FMA otherwise.
-// TSM2X_CONSUMER=fma|dmma|ffma2 in the environment overrides (ablation runs).
-enum ConsumerKind { kFma = 0, kDmma = 1, kFfma2 = 2, kNull = 3 };
+// Consumer choice (tsm2r_tma.cuh, tsm2r_tc32.cuh): DMMA for fp64 passes of width 8 or 16 (fewer
+// issue slots and less energy per FMA than DFMA), split-precision tf32 tensor cores for fp32
+// 16-column passes, packed FFMA2 for other fp32 widths, plain FMA otherwise.
+// TSM2X_CONSUMER=fma|dmma|ffma2|tc in the environment overrides (ablation runs).
+enum ConsumerKind { kFma = 0, kDmma = 1, kFfma2 = 2, kNull = 3, kTc = 4 };
 
 static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
   static const int env = [] {
@@ -297,6 +325,7 @@ static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
     if (!strcmp(e, "fma")) return (int)kFma;
     if (!strcmp(e, "dmma")) return (int)kDmma;
     if (!strcmp(e, "ffma2")) return (int)kFfma2;
+    if (!strcmp(e, "tc")) return (int)kTc;  // fp32: split-precision tf32 on tcgen05 (tsm2r_tc32.cuh)
     if (!strcmp(e, "null")) return (int)kNull;  // diagnostic: pipeline only, wrong results
     return -1;
   }();
@@ -305,16 +334,21 @@ static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
                             : (tu.consumer == 1   ? kFma
                                : tu.consumer == 2 ? kDmma
                                : tu.consumer == 3 ? kFfma2
+                               : tu.consumer == 4 ? kTc
                                                   : -1);
   const bool dmma_ok = eb == 8 && (nt == 8 || nt == 16);
   const bool ffma2_ok = eb == 4 && nt >= 2;
   if (want == kFma) return kFma;
   if (want == kDmma) return dmma_ok ? kDmma : kFma;
   if (want == kFfma2) return ffma2_ok ? kFfma2 : kFma;
+  if (want == kTc) return eb == 4 ? kTc : (dmma_ok ? kDmma : kFma);
   // fp64 8- and 16-column passes: DMMA. At n=8 DMMA and DFMA take the same time under the 1000 W
   // cap on most parts (DMMA runs ~300 MHz higher for the same energy) and DMMA is up to 3 %
   // faster on others (profiles/envab_r01.json); at n=16 DMMA wins outright
   if (dmma_ok) return kDmma;
+  // fp32 16-column passes: split-precision tf32 on the tensor cores (tsm2r_tc32.cuh; taken when
+  // the layout allows, else FFMA2): -13 % burst, -13 % sustained vs FFMA2 (profiles/envab_r01.json)
+  if (eb == 4 && nt == 16) return kTc;
   if (ffma2_ok) return kFfma2;
   return kFma;
 }
@@ -431,6 +465,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   // DMMA: the 512-row geometries (8 warps x 2 rows or 16 warps x 1 row); FFMA2: the default one
   if (kind == kDmma && !(RPT * CW == 16 && (CW == 8 || CW == 16))) kind = kFma;
   if (kind == kFfma2 && (RPT != Vec<T>::N || CW != 8)) kind = kFma;
+  if (kind == kTc) kind = (sizeof(T) == 4 && RPT == Vec<T>::N && CW == 8 && NT >= 2) ? kFfma2 : kFma;  // tc path not taken
   const size_t bt_bytes = align_up((size_t)kpad * NT * sizeof(T), 256);
   TSM2X_TRY(ws_reserve(ws, bt_bytes + acc_bytes, (size_t)it.num_rb + 8, s));
   a.tickets = reinterpret_cast<unsigned*>(ws->counters + 8);  // zero between launches
@@ -484,6 +519,105 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
     const int64_t tot = m * w;
     const unsigned grid = (unsigned)std::min<int64_t>((tot + 255) / 256, (int64_t)di.sms * 8);
     tsm2_finalize<T><<<grid, 256, 0, s>>>(a.acc, a.ldacc, C, ldc, m, w, a.c_is_zero);
+    TSM2X_TRY(check_launch("tsm2_finalize"));
+  }
+  return TSM2X_OK;
+}
+
+// fp32 on the tensor cores (tsm2r_tc32.cuh): split-precision tf32, one 16-column pass (w <= 16).
+// Dynamic items as run_tsm2r_tma; split row blocks combine with fp64 reductions into the fp64
+// accumulator (+ tsm2_finalize), single-chunk row blocks store C directly.
+static bool tc32_ok(const float* A, int64_t m, int64_t k, int64_t lda) {
+  return aligned16(A) && lda % 4 == 0 && lda >= (int64_t)align_up((size_t)m, 32) && m < (int64_t(1) << 31) &&
+         k < (int64_t(1) << 31);
+}
+
+static int run_tsm2r_tc32(const DevInfo& di, Workspace* ws, int64_t m, int64_t k, int w, const float* A, int64_t lda,
+                          const float* B, int64_t ldb, float* C, int64_t ldc, bool c_is_zero, cudaStream_t s) {
+  using Cfg = Tc32Cfg;
+  const Tuning tu = current_tuning();
+  DynArgs<float> a;
+  a.C = C;
+  a.ldc = ldc;
+  a.m = m;
+  a.k = k;
+  a.w = w;
+  a.c_is_zero = c_is_zero ? 1 : 0;
+  a.vec_c = 0;
+  Items& it = a.it;
+  int64_t G;
+  make_items(di.sms, m, k, sizeof(float), Cfg::R, Cfg::KC, 16, tu, &it, &G);
+  const bool split = it.nch() > 1;
+  const int64_t nstages = (k + Cfg::KC - 1) / Cfg::KC;
+  a.ldacc = (int64_t)it.num_rb * Cfg::R;
+  a.ordered = 0;
+  const size_t acc_bytes = split ? (size_t)a.ldacc * 16 * sizeof(double) : 0;
+  const size_t bt_bytes = align_up((size_t)nstages * Cfg::B_BYTES, 256);
+  TSM2X_TRY(ws_reserve(ws, bt_bytes + acc_bytes, (size_t)it.num_rb + 8, s));
+  a.tickets = reinterpret_cast<unsigned*>(ws->counters + 8);
+  a.Bt = reinterpret_cast<const float*>(ws->buf);
+  a.acc = acc_bytes ? reinterpret_cast<double*>(static_cast<char*>(ws->buf) + bt_bytes) : nullptr;
+  a.queue = reinterpret_cast<unsigned long long*>(ws->counters);
+  {
+    const int64_t tot = nstages * 512 + (a.acc ? a.ldacc * w : 0);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, (int64_t)di.sms * 16));
+    prep_tc32<<<grid, 256, 0, s>>>(B, ldb, k, nstages, w, const_cast<float*>(a.Bt), a.acc, a.ldacc, a.ldacc, w);
+    TSM2X_TRY(check_launch("prep_tc32"));
+  }
+#ifdef TSM2X_TC32_DIAG
+  // diagnostics (TSM2X_TC_DIAG=<skip bits>, any value enables the cycle counters; printed to stderr)
+  static const int env_diag = [] {
+    const char* e = getenv("TSM2X_TC_DIAG");
+    return e ? atoi(e) + 0x10000 : 0;
+  }();
+  static unsigned long long* dbg = nullptr;
+  if (env_diag) {
+    if (!dbg) TSM2X_CUDA(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
+    TSM2X_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), s));
+    a.diag = env_diag & 0xffff;
+    a.dbg = dbg;
+  }
+#else
+  constexpr int env_diag = 0;
+  unsigned long long* dbg = nullptr;
+#endif
+  alignas(64) CUtensorMap tmap;
+  TSM2X_TRY(encode_a_map_tc32(&tmap, A, m, k, lda));
+  auto kern = tsm2r_stream_tc32;
+  TSM2X_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  const bool timed = t_ev_start && t_ev_stop;
+  if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)G);
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TSM2X_CUDA(cudaLaunchKernelEx(&cfg, kern, a, tmap));
+  TSM2X_TRY(check_launch("tsm2r_stream_tc32"));
+  if (env_diag) {
+    unsigned long long h[16];
+    TSM2X_CUDA(cudaMemcpyAsync(h, dbg, sizeof h, cudaMemcpyDeviceToHost, s));
+    TSM2X_CUDA(cudaStreamSynchronize(s));
+    const double ns = h[4] ? (double)h[4] : 1.0;
+    fprintf(stderr,
+            "{\"tc32_diag\": %d, \"stages\": %llu, \"mma_wait_full\": %.0f, \"mma_wait_lo\": %.0f, \"mma_issue\": %.0f, "
+            "\"mma_wait_acc\": %.0f, \"conv_wait_full\": %.0f, \"conv_wait_lo_empty\": %.0f, \"conv_convert\": %.0f, "
+            "\"conv_epilogue\": %.0f}\n",
+            env_diag & 0xffff, h[4], h[0] / ns, h[1] / ns, h[2] / ns, h[3] / ns, h[8] / ns, h[9] / ns, h[10] / ns, h[11] / ns);
+  }
+  if (timed) {
+    TSM2X_CUDA(cudaEventRecord(t_ev_stop, s));
+    t_ev_start = t_ev_stop = nullptr;
+  }
+  if (split) {
+    const int64_t tot = m * w;
+    const unsigned grid = (unsigned)std::min<int64_t>((tot + 255) / 256, (int64_t)di.sms * 8);
+    tsm2_finalize<float><<<grid, 256, 0, s>>>(a.acc, a.ldacc, C, ldc, m, w, a.c_is_zero);
     TSM2X_TRY(check_launch("tsm2_finalize"));
   }
   return TSM2X_OK;
@@ -624,6 +758,14 @@ static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m,
   const int combine = current_tuning().combine;
   if (tma && combine == 3) return run_tsm2r_tma_static<T, NT>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, s);
   const bool ordered = combine == 1 || (combine == 0 && deterministic);
+  if constexpr (sizeof(T) == 4 && (NT == 16 || NT == 8)) {
+    // fp32: the tensor-core consumer when chosen (TSM2X_CONSUMER=tc / tuning consumer 4) and the
+    // layout allows the 3-D TMA view; the deterministic (ordered) combine stays on FFMA2
+    if (tma && !ordered && pick_consumer_rt(4, NT, true, current_tuning()) == kTc &&
+        tc32_ok(reinterpret_cast<const float*>(A), m, k, lda))
+      return run_tsm2r_tc32(di, ws, m, k, w, reinterpret_cast<const float*>(A), lda,
+                            reinterpret_cast<const float*>(B), ldb, reinterpret_cast<float*>(C), ldc, c_is_zero, s);
+  }
   if (tma) {
     // rows per consumer thread (row-block height R = 256 * rpt): TSM2X_RPT overrides for
     // experiments on fp64 8-column passes (1, 2, 4, 8); the default is one 16-byte vector's worth
@@ -1268,6 +1410,24 @@ int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, 
   const Tuning tu = current_tuning();
   Items it;
   int64_t G;
+  if (eb == 4 && nt == 16 && !determ && tu.combine != 1 && pick_consumer_rt(4, nt, true, tu) == kTc &&
+      a_aligned16 && lda % 4 == 0 && lda >= (int64_t)align_up((size_t)m, 32) && k < (int64_t(1) << 31)) {
+    // fp32 16-column passes on the tensor cores (run_tsm2r_tc32)
+    out->rows_per_block = Tc32Cfg::R;
+    out->cols_per_stage = Tc32Cfg::KC;
+    out->stages = Tc32Cfg::STAGES;
+    make_items(sms, m, k, eb, Tc32Cfg::R, Tc32Cfg::KC, nt, tu, &it, &G);
+    out->grid = G;
+    out->items = it.total;
+    out->nbig = it.nbig;
+    out->kbig = it.kbig;
+    out->nsmall = it.nsmall;
+    out->ksmall = it.ksmall;
+    out->batch = it.batch;
+    out->consumer = 1 + kTc;
+    out->deterministic = it.nch() == 1 ? 1 : 0;
+    return TSM2X_OK;
+  }
   make_items(sms, m, k, eb, R, out->cols_per_stage, nt, tu, &it, &G);
   out->grid = G;
   out->items = it.total;
@@ -1277,6 +1437,7 @@ int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, 
   out->ksmall = it.ksmall;
   out->batch = it.batch;
   out->consumer = 1 + pick_consumer_rt(eb, nt, it.nch() > 1, tu);
+  if (out->consumer == 1 + kTc) out->consumer = 1 + (nt >= 2 ? kFfma2 : kFma);  // tc path not taken
   out->deterministic = (it.nch() == 1 || tu.combine == 1 || (tu.combine == 0 && determ)) ? 1 : 0;
   return TSM2X_OK;
 }

@@ -16,7 +16,8 @@ tcf         rows per thread (TSM2L)         ``batch_kb``: A bytes per queue grab
                                             single-chunk row blocks
 (new)       work-item sizes                 ``small_kb``/``big_kb``/``tail_pct``: dynamic
                                             queue granularity (tail vs. combine traffic)
-(new)       consumer datapath               FMA / DMMA (fp64 tensor MMA) / FFMA2 (packed fp32)
+(new)       consumer datapath               FMA / DMMA (fp64 tensor MMA) / FFMA2 (packed fp32) /
+                                            TC (fp32: split tf32 on tcgen05, tsm2r_tc32.cuh)
 ==========  ==============================  =================================================
 
 :func:`plan` reports what the library will launch for a shape; :func:`tune_tsm2r` /
@@ -34,13 +35,15 @@ from typing import Dict, List, Optional
 
 from . import _lib
 
-CONSUMERS = {0: "auto", 1: "fma", 2: "dmma", 3: "ffma2"}
+CONSUMERS = {0: "auto", 1: "fma", 2: "dmma", 3: "ffma2", 4: "tc"}  # tsm2x_tuning.consumer
+PLAN_CONSUMERS = {0: "none", 1: "fma", 2: "dmma", 3: "ffma2", 4: "null", 5: "tc"}  # tsm2x_plan.consumer
 IMPLS = {v: k for k, v in _lib.IMPL.items()}
 
 # The library's built-in defaults (tsm2x.cu make_items / pick_consumer_rt), stated here for
 # reporting; 0 in a Tuning means "use these".
 B200_DEFAULTS = {
-    "consumer": "auto: DMMA for fp64 8- and 16-column passes; FFMA2 for fp32 n >= 2; else FMA "
+    "consumer": "auto: DMMA for fp64 8- and 16-column passes; split-precision tf32 on the tensor cores (tc) "
+                "for fp32 16-column passes; FFMA2 for other fp32 n >= 2; else FMA "
                 "(sustained A/B under the 1000 W cap: profiles/envab_r01.json)",
     "small_kb": "min(512 (1024 for 16-column passes), max(64, per-CTA share / 48))",
     "big_kb": "min(4096, max(small, per-CTA share / 6))",
@@ -88,7 +91,7 @@ def plan(precision: str, m: int, k: int, n: int, lda: Optional[int] = None, alig
                                           ctypes.byref(out)))
     d = {f: getattr(out, f) for f, _ in _lib.Plan._fields_}
     d["impl"] = IMPLS.get(d["impl"], d["impl"])
-    d["consumer"] = CONSUMERS.get(d["consumer"], d["consumer"])
+    d["consumer"] = PLAN_CONSUMERS.get(d["consumer"], d["consumer"])
     # the paper's vocabulary, for tune-style reporting
     d["t1"] = d["rows_per_block"]
     d["t2"] = d["cols_per_pass"]

@@ -391,7 +391,7 @@ def test_config4_fp32_sampled():
         _check(Ch[r0:r0 + 128], ref, k, "single", what=r0)
 
 
-@pytest.mark.parametrize("consumer", ["fma", "dmma", "ffma2", "dmma/cw16", "fma/cw16"])
+@pytest.mark.parametrize("consumer", ["fma", "dmma", "ffma2", "tc", "dmma/cw16", "fma/cw16"])
 def test_consumer_policies_subprocess(consumer):
     """Each TMA consumer policy (TSM2X_CONSUMER override; "/cw16" = the 16-consumer-warp x 1-row
     geometry, TSM2X_CW=16 TSM2X_RPT=1) on split and single-chunk shapes."""
@@ -435,3 +435,92 @@ def test_run_native_multi_device_shards(devices):
         out = tsm.run_native_multi(tsm.Variant.V3, tsm.Matrix.from_2d(A, "double"), tsm.Matrix.from_2d(B, "double"),
                                    tsm.Matrix.from_2d(C0, "double"), tsm.KernelParams(t2=min(4, n)), devices)
         _check(out.to_2d(), naive_gemm(A, B, C0), k, "double", what=(devices, m, k, n))
+
+
+@pytest.mark.parametrize("c_zero", [False, True])
+def test_tc32_tensor_core_shapes(c_zero):
+    """fp32 16-column passes on the tensor cores (tsm2r_stream_tc32, split-precision tf32): ragged
+    rows (m % 32, m % 512), ragged k (k % 16), n = 9..16, split and single-chunk row blocks,
+    C += A.B and the zero-C contract."""
+    import torch
+    tsm = _tsm()
+    from paper_2002_03258_b200 import tuning
+    rng = np.random.default_rng(11 + c_zero)
+    for (m, k, n) in [(1, 1, 16), (31, 7, 9), (33, 17, 12), (513, 100, 16), (4113, 5000, 16), (1024, 33, 15),
+                      (70001, 16, 16), (2048, 40000, 16)]:
+        assert tuning.plan("single", m, k, n)["consumer"] == "tc", (m, k, n)
+        A = tsm.colmajor_empty(m, k, torch.float32, "cuda")
+        A.copy_(torch.from_numpy(rng.standard_normal((m, k)).astype(np.float32)))
+        B = tsm.colmajor_empty(k, n, torch.float32, "cuda")
+        B.copy_(torch.from_numpy(rng.standard_normal((k, n)).astype(np.float32)))
+        C0 = np.zeros((m, n), np.float32) if c_zero else rng.standard_normal((m, n)).astype(np.float32)
+        C = tsm.colmajor_empty(m, n, torch.float32, "cuda")
+        C.copy_(torch.from_numpy(C0))
+        tsm.gemm(A, B, C, variant="l-opt2" if c_zero else "v3", c_is_zero=c_zero)
+        ref = naive_gemm(A.cpu().numpy().astype(np.float64), B.cpu().numpy().astype(np.float64), C0.astype(np.float64))
+        out = C.cpu().numpy().astype(np.float64)
+        assert rel_frobenius(out, ref) <= 1e-5, (m, k, n, rel_frobenius(out, ref))
+        # elementwise: within fp32 accumulation error of the |A||B| scale
+        scale = np.abs(A.cpu().numpy()).astype(np.float64) @ np.abs(B.cpu().numpy()).astype(np.float64) + np.abs(C0)
+        assert np.max(np.abs(out - ref) / scale) <= 4 * k * np.finfo(np.float32).eps + 1e-6, (m, k, n)
+
+
+def test_tc32_exact_cases():
+    """Tensor-core fp32 path: small integers are exact; an identity A returns B to within the
+    split's one dropped term (lo(B) enters as tf32: 2^-22 relative) — the bitwise identity of the
+    reference's tests (test_kernels.py:20-44) is fp64, which stays bitwise (golden identity_v3)."""
+    import torch
+    tsm = _tsm()
+    rng = np.random.default_rng(3)
+    k, n = 256, 16
+    Bh = rng.standard_normal((k, n)).astype(np.float32)
+    A = tsm.colmajor_empty(k, k, torch.float32, "cuda")
+    A.copy_(torch.eye(k))
+    B = tsm.colmajor_empty(k, n, torch.float32, "cuda")
+    B.copy_(torch.from_numpy(Bh))
+    C = tsm.colmajor_empty(k, n, torch.float32, "cuda")
+    C.zero_()
+    tsm.gemm(A, B, C)
+    assert np.max(np.abs(C.cpu().numpy() - Bh) / np.abs(Bh)) <= 2.0 ** -21
+    Ai = rng.integers(-8, 8, (1000, 640)).astype(np.float32)
+    Bi = rng.integers(-8, 8, (640, 16)).astype(np.float32)
+    A = tsm.colmajor_empty(1000, 640, torch.float32, "cuda")
+    A.copy_(torch.from_numpy(Ai))
+    B = tsm.colmajor_empty(640, 16, torch.float32, "cuda")
+    B.copy_(torch.from_numpy(Bi))
+    C = tsm.colmajor_empty(1000, 16, torch.float32, "cuda")
+    C.zero_()
+    tsm.gemm(A, B, C)
+    assert np.array_equal(C.cpu().numpy(), Ai @ Bi)
+
+
+def test_tc32_nonfinite_inputs_propagate():
+    """Non-finite entries of A or B give non-finite outputs in exactly the reference's positions
+    (an infinity may surface as NaN on the tensor-core path: inf * 0 in the split cross terms);
+    deterministic=True (FFMA2, IEEE fp32 FMA chain) matches the reference's inf/NaN kinds too."""
+    import torch
+    tsm = _tsm()
+    rng = np.random.default_rng(5)
+    m, k, n = 600, 300, 16
+    Ah = rng.random((m, k)).astype(np.float32)
+    Bh = rng.random((k, n)).astype(np.float32)
+    Ah[5, 7] = np.inf
+    Ah[100, 0] = -np.inf
+    Ah[300, 299] = np.nan
+    Bh[11, 3] = np.inf
+    with np.errstate(invalid="ignore", over="ignore"):
+        ref = Ah.astype(np.float64) @ Bh.astype(np.float64)
+    for det in (False, True):
+        A = tsm.colmajor_empty(m, k, torch.float32, "cuda")
+        A.copy_(torch.from_numpy(Ah))
+        B = tsm.colmajor_empty(k, n, torch.float32, "cuda")
+        B.copy_(torch.from_numpy(Bh))
+        C = tsm.colmajor_empty(m, n, torch.float32, "cuda")
+        C.zero_()
+        tsm.gemm(A, B, C, deterministic=det)
+        out = C.cpu().numpy()
+        assert np.array_equal(~np.isfinite(out), ~np.isfinite(ref)), det
+        fin = np.isfinite(ref)
+        assert rel_frobenius(out[fin].astype(np.float64), ref[fin]) <= 1e-5
+        if det:
+            assert np.array_equal(np.isnan(out), np.isnan(ref))

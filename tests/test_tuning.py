@@ -8,7 +8,7 @@ from paper_2002_03258_b200 import tuning
 
 def test_plan_config2_tsm2r():
     p = tuning.plan("double", 30720, 30720, 8)
-    assert p["impl"] == "tma" and p["consumer"] == "fma"
+    assert p["impl"] == "tma" and p["consumer"] == "dmma"  # fp64 8-column passes (envab_r01.json)
     assert p["t1"] == 512 and p["t2"] == 8 and p["t3"] == 48
     assert p["grid"] <= 148 and p["items"] >= 24 * p["grid"] // 2
     assert p["nbig"] > 0 and p["nsmall"] > 0 and p["batch"] == 1
@@ -20,12 +20,17 @@ def test_plan_tsm2l_single_chunk():
     p = tuning.plan("double", 1 << 24, 16, 16)
     assert p["impl"] == "tma" and p["consumer"] == "dmma"  # fp64 16-column passes (abtest_r01e.json)
     assert p["nbig"] == 0 and p["nsmall"] == 1 and p["batch"] > 1
-    assert tuning.plan("double", 1 << 24, 16, 8)["consumer"] == "fma"
+    assert tuning.plan("double", 1 << 24, 16, 8)["consumer"] == "dmma"
+    assert tuning.plan("double", 1 << 24, 16, 4)["consumer"] == "fma"
 
 
 def test_plan_fp32_and_wide():
     p = tuning.plan("single", 32768, 32768, 16)
+    assert p["consumer"] == "tc" and p["t1"] == 512 and p["cols_per_stage"] == 16  # tcgen05 split tf32
+    assert tuning.plan("single", 32768, 32768, 8)["consumer"] == "ffma2"
+    p = tuning.plan("single", 32768, 32768, 16, deterministic=True)  # ordered combine stays on FFMA2
     assert p["consumer"] == "ffma2" and p["t1"] == 1024
+    assert tuning.plan("single", 1001, 5000, 16, lda=1004)["consumer"] == "ffma2"  # lda < roundup(m, 32)
     assert tuning.plan("double", 1000, 1000, 40)["passes"] == 3
 
 

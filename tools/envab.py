@@ -23,6 +23,8 @@ CFGS = {
     "r2": (30720, 30720, 2, "double", False),
     "l16": (1 << 24, 16, 16, "double", True),
     "f16": (32768, 32768, 16, "single", False),
+    "f8": (32768, 32768, 8, "single", False),
+    "l16f": (1 << 24, 16, 16, "single", True),
 }
 
 
