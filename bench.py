@@ -62,6 +62,17 @@ def algorithmic(m, k, n, eb, c_is_zero):
     return flops, byts
 
 
+def kernel_name(prec, m, k, n, c_is_zero):
+    """The dominant kernel this workload launches, from the library's own plan (tsm2x_plan_for)."""
+    from paper_2002_03258_b200 import tuning
+    p = tuning.plan(prec, m, k, n)
+    if p["consumer"] == "tc":
+        return ("tsm2r_stream_tc32 (tcgen05 kind::tf32, split precision A.[B|lo B] + lo(A).B, accumulators in TMEM; "
+                "dynamic items)")
+    return f"tsm2r_stream_tma ({p['consumer']} consumer; dynamic items" + \
+        ("; single-chunk row blocks)" if p["nbig"] == 0 else ")")
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -329,7 +340,7 @@ def run_ours(args, wl):
             "GBps": round(gbps, 1),
             "roofline": {"bound": "hbm", "achieved": round(kern_gbps, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(kern_gbps / peak, 4), "traffic": traffic,
-                         "kernel": "tsm2r_stream_tma (dynamic items; single-chunk row blocks when k is small)",
+                         "kernel": kernel_name(prec, m, k, n, c_is_zero),
                          "kernel_ms": round(kern_ms, 5), "algorithmic_bytes_per_launch": byts,
                          "peak_source": peak_src,
                          "read_stream_ceiling_gbs": 7300.0,

@@ -217,11 +217,12 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
           int64_t rb, col0, col1;
           a.it.decode(item, a.k, &rb, &col0, &col1);
           const uint32_t tx = (uint32_t)(Cfg::A_BYTES + Cfg::B_BYTES);  // OOB rows/columns are zero-filled
+          const int64_t nst = (col1 - col0 + KC - 1) / KC;
           for (int64_t col = col0; col < col1; col += KC, ++it) {
             const int s = it % STAGES;
             const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
             mbar_wait(&empty[s], ph ^ 1u);
-            meta[s] = make_longlong2(rb, item);
+            meta[s] = make_longlong2(rb | (nst << 32), item);  // read by the consumers once per item
             mbar_arrive_expect_tx(&full[s], tx);
             tma_load_3d(sA + (size_t)s * Cfg::A_BYTES, &tmA, 0, (int)col, (int)(rb * (R / 32)), &full[s], pol);
             bulk_g2s(sB + (size_t)s * Cfg::B_BYTES, reinterpret_cast<const unsigned char*>(a.Bt) + (col / KC) * Cfg::B_BYTES,
@@ -254,6 +255,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
     constexpr uint32_t B_HI = (512u >> 4) | (1u << 14) | (4u << 29);
     constexpr uint32_t A_LBO = (2048u >> 4) << 16;  // between 32-row chunks
     int64_t cur = -1;
+    int left = 0;           // stages of the current item still to come
     int seg = -1, sin = 0;  // segment (accumulator buffer seg & 1) and stages issued into it
     uint32_t acc0 = 1;
     TC32_DIAG(unsigned long long c_full = 0, c_lo = 0, c_issue = 0, c_acc = 0, n_st = 0;)
@@ -262,14 +264,17 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
       TC32_DIAG(const unsigned long long t0c = clock64();)
       mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
       TC32_DIAG(const unsigned long long t1c = clock64(); c_full += t1c - t0c;)
-      const longlong2 md = meta[s];
-      if (md.y != cur || sin == Cfg::SEG) {
+      if (left == 0 || sin == Cfg::SEG) {
         // new item, or SEG stages into the current segment: close the segment (its accumulators
         // go to the converters, which fold them into fp64) and start the next one from zero
         if (cur >= 0 && elect_one()) tc_commit(&acc_full[seg & 1]);
         __syncwarp();
-        if (md.y < 0) break;
-        cur = md.y;
+        if (left == 0) {
+          const longlong2 md = meta[s];
+          if (md.y < 0) break;
+          cur = md.y;
+          left = (int)(md.x >> 32);
+        }
         ++seg;
         sin = 0;
         TC32_DIAG(const unsigned long long ta = clock64();)
@@ -278,6 +283,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
         acc0 = 0;
       }
       ++sin;
+      --left;
       const int slot = it % Cfg::LO_SLOTS;
       TC32_DIAG(const unsigned long long t2c = clock64();)
       mbar_wait(&lo_full[slot], (uint32_t)(it / Cfg::LO_SLOTS) & 1u);
@@ -324,6 +330,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
     const int t0 = 2 * (cw >> 2);   // tiles t0, t0 + 1
     const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
     int64_t cur = -1, cur_rb = 0;
+    int left = 0;                      // stages of the current item still to come
     int seg = -1, pend = -1, sin = 0;  // current segment, segment awaiting its drain, stages in segment
     // this thread's row of tiles t0, t0 + 1: running sums of the drained segments (fp32 with
     // round-to-nearest over ~16 segment values; fp64 would not fit the 168-register budget)
@@ -380,13 +387,14 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
       TC32_DIAG(const unsigned long long t0c = clock64();)
       mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
       TC32_DIAG(const unsigned long long t1c = clock64(); c_full += t1c - t0c;)
-      const longlong2 md = meta[s];
-      if (md.y != cur) {
+      if (left == 0) {
+        const longlong2 md = meta[s];
         if (cur >= 0) finish_item();
         TC32_DIAG(c_epi += clock64() - t1c;)
         if (md.y < 0) break;
         cur = md.y;
-        cur_rb = md.x;
+        cur_rb = md.x & 0xffffffffll;
+        left = (int)(md.x >> 32);
         ++seg;
         sin = 0;
       } else if (sin == Cfg::SEG) {
@@ -399,6 +407,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
         sin = 0;
       }
       ++sin;
+      --left;
       const int slot = it % Cfg::LO_SLOTS;
       TC32_DIAG(const unsigned long long t2c = clock64();)
       if (it >= Cfg::LO_SLOTS) {  // the slot's previous stage (it - LO_SLOTS) has finished its MMAs

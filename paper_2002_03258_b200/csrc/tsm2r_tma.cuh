@@ -28,6 +28,13 @@
 #include "common.cuh"
 #include "tsm2r_stream.cuh"
 
+// Diagnostic build (nvcc -DTSM2X_TC32_DIAG, `make diag`): per-stage cycle counters.
+#ifdef TSM2X_TC32_DIAG
+#define KDIAG(...) __VA_ARGS__
+#else
+#define KDIAG(...)
+#endif
+
 namespace tsm2x {
 
 template <typename T, int NT, int RPT_ = Vec<T>::N, int CW_ = 8>
@@ -494,7 +501,8 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
   T* sB = reinterpret_cast<T*>(smem + STAGES * Cfg::A_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * (Cfg::A_BYTES + Cfg::B_BYTES_PAD));
   uint64_t* empty = full + STAGES;
-  longlong2* meta = reinterpret_cast<longlong2*>(empty + STAGES);  // (row block, item id) per stage; id -1 = end
+  // per stage: (row block | stages in the item << 32, item id); id -1 = end
+  longlong2* meta = reinterpret_cast<longlong2*>(empty + STAGES);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
@@ -523,11 +531,12 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
           const int64_t row_base = rb * R;
           const int nbox = (int)min64(Cfg::NBOX, (a.m - row_base + Cfg::BOX - 1) / Cfg::BOX);
           const uint32_t tx = (uint32_t)(nbox * Cfg::BOX * KC * (int)sizeof(T) + Cfg::B_BYTES);
+          const int64_t nst = (col1 - col0 + KC - 1) / KC;
           for (int64_t col = col0; col < col1; col += KC, ++it) {
             const int s = it % STAGES;
             const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
             mbar_wait(&empty[s], ph ^ 1u);
-            meta[s] = make_longlong2(rb, item);
+            meta[s] = make_longlong2(rb | (nst << 32), item);
             mbar_arrive_expect_tx(&full[s], tx);
             for (int b = 0; b < nbox; ++b)
               tma_load_2d(sA + (size_t)s * Cfg::A_ELEMS + b * (Cfg::BOX * KC), &tmA, (int)(row_base + b * Cfg::BOX),
@@ -557,27 +566,42 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
   Consumer cons;
   cons.init(threadIdx.x - 32);
   int64_t cur = -1, cur_rb = 0;
+  int left = 0;  // stages of the current item still to come: meta is read once per item (an LDS
+                 // per stage queued behind the fragment loads of all warps cost ~15 % of issue)
+  KDIAG(unsigned long long c_wait = 0, c_stage = 0, c_fin = 0, n_st = 0;)
   for (int it = 0;; ++it) {
     const int s = it % STAGES;
     const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+    KDIAG(const unsigned long long t0c = clock64();)
     mbar_wait(&full[s], ph);
-    const longlong2 md = meta[s];
-    if (md.y < 0) {  // end marker (a CTA may get no item at all: test before comparing with cur)
-      if (cur >= 0) cons.finish(a, cur_rb, cur);
-      break;
-    }
-    if (md.y != cur) {
+    KDIAG(const unsigned long long t1c = clock64(); c_wait += t1c - t0c;)
+    if (left == 0) {
+      const longlong2 md = meta[s];
+      if (md.y < 0) {  // end marker (a CTA may get no item at all)
+        if (cur >= 0) cons.finish(a, cur_rb, cur);
+        break;
+      }
       if (cur >= 0) {
         cons.finish(a, cur_rb, cur);
         cons.zero();
       }
       cur = md.y;
-      cur_rb = md.x;
+      cur_rb = md.x & 0xffffffffll;
+      left = (int)(md.x >> 32);
     }
+    --left;
+    KDIAG(const unsigned long long t2c = clock64(); c_fin += t2c - t1c;)
     cons.stage(sA + (size_t)s * Cfg::A_ELEMS, sB + (size_t)s * (Cfg::B_BYTES_PAD / sizeof(T)));
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+    KDIAG(c_stage += clock64() - t2c; ++n_st;)
   }
+  KDIAG(if (a.dbg && threadIdx.x == 32) {
+    atomicAdd(a.dbg + 0, c_wait);
+    atomicAdd(a.dbg + 1, c_stage);
+    atomicAdd(a.dbg + 2, c_fin);
+    atomicAdd(a.dbg + 4, n_st);
+  })
 }
 
 // Bt in DMMA fragment order: for each group of 4 B rows (kg) and N tile (nt), the 32 values in

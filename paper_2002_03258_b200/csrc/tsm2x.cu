@@ -499,6 +499,15 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
       TSM2X_TRY(check_launch("prep_dyn"));
     }
   }
+#ifdef TSM2X_TC32_DIAG
+  static unsigned long long* dbg = nullptr;
+  const bool diag = getenv("TSM2X_TC_DIAG") != nullptr;
+  if (diag) {
+    if (!dbg) TSM2X_CUDA(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
+    TSM2X_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), s));
+    a.dbg = dbg;
+  }
+#endif
   alignas(64) CUtensorMap tmap;
   TSM2X_TRY(encode_a_map(&tmap, A, m, k, lda, eb, Cfg::BOX, Cfg::KC));
   const bool timed = t_ev_start && t_ev_stop;
@@ -511,6 +520,16 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
     TSM2X_TRY((launch_tma_kernel<T, NT, kNull, RPT, CW>(a, tmap, G, s)));
   else
     TSM2X_TRY((launch_tma_kernel<T, NT, kFma, RPT, CW>(a, tmap, G, s)));
+#ifdef TSM2X_TC32_DIAG
+  if (diag) {
+    unsigned long long h[16];
+    TSM2X_CUDA(cudaMemcpyAsync(h, dbg, sizeof h, cudaMemcpyDeviceToHost, s));
+    TSM2X_CUDA(cudaStreamSynchronize(s));
+    const double ns = h[4] ? (double)h[4] : 1.0;
+    fprintf(stderr, "{\"tma_diag\": \"consumer %d\", \"stages\": %llu, \"wait_full\": %.0f, \"stage\": %.0f, \"finish\": %.0f}\n",
+            kind, h[4], h[0] / ns, h[1] / ns, h[2] / ns);
+  }
+#endif
   if (timed) {
     TSM2X_CUDA(cudaEventRecord(t_ev_stop, s));
     t_ev_start = t_ev_stop = nullptr;

@@ -8,7 +8,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   --log-file gpurun_out/launches_${TAG}.csv python bench.py --steps 20 --warmup 3 --e2e-steps 0 --no-cpu-baseline \
   > gpurun_out/ncu_launch_stdout.txt 2>&1
 for wl in $WLS; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tsm2r_stream_tma -s 5 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tsm2r_stream_(tma|tc32)" -s 5 -c 1 \
     -o gpurun_out/prof_${TAG}_${wl} python bench.py --workload $wl --steps 8 --warmup 3 --e2e-steps 0 --no-cpu-baseline \
     > gpurun_out/ncu_full_${wl}.txt 2>&1
   ncu -i gpurun_out/prof_${TAG}_${wl}.ncu-rep --page raw --csv > gpurun_out/prof_${TAG}_${wl}.raw.csv 2>/dev/null

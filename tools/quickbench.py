@@ -31,7 +31,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--impls", default="ldg,tma")
     ap.add_argument("--configs", default="r2,r4,r8,r16,l16,f16,r8_4096")
+    ap.add_argument("--tuning", default="", help="e.g. small_kb=2048,tail_pct=10 (paper_2002_03258_b200.tuning)")
     args = ap.parse_args()
+    if args.tuning:
+        from paper_2002_03258_b200 import tuning
+        kw = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in args.tuning.split(",")}
+        tuning.set_tuning(tuning.Tuning(**kw))
     cfgs = {
         "r2": (30720, 30720, 2, torch.float64, "v3"),
         "r4": (30720, 30720, 4, torch.float64, "v3"),
