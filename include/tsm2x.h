@@ -122,7 +122,8 @@ int tsm2x_fill_uniform(int precision, int64_t rows, int64_t cols, void* ptr, int
  * (reference tuner.py:218-363). Process-wide knobs; 0 = the shipped B200 default. */
 typedef struct tsm2x_tuning {
   int32_t consumer;   /* 0 auto, 1 FMA, 2 DMMA (fp64, 8/16 columns), 3 FFMA2 (fp32),
-                         4 TC (fp32 16-column passes: split-precision tf32 on tcgen05)        */
+                         4 TC (fp32 16-column passes: split-precision tf32 on tcgen05),
+                         5 DMMA with the k-step software-pipelined loop (experimental)       */
   int32_t small_kb;   /* KB of A per "small" work item (end of the queue)                     */
   int32_t big_kb;     /* KB of A per "big" work item                                          */
   int32_t tail_pct;   /* % of each row block's columns handed out as small items              */
@@ -136,7 +137,8 @@ int tsm2x_get_tuning(tsm2x_tuning* out);
 /* What a tsm2x_run_ex call with these arguments would launch (first 16-column pass). */
 typedef struct tsm2x_plan {
   int32_t impl;            /* enum tsm2x_impl actually used (AUTO resolved)                    */
-  int32_t consumer;        /* 1 FMA, 2 DMMA, 3 FFMA2, 5 TC (tensor-core fp32) (TMA kernels), 0 otherwise */
+  int32_t consumer;        /* 1 FMA, 2 DMMA, 3 FFMA2, 5 TC (tensor-core fp32), 6 DMMA pipelined
+                              (TMA kernels), 0 otherwise                                       */
   int32_t rows_per_block;  /* R: rows per row block            (the paper's t1 analogue)      */
   int32_t cols_per_pass;   /* NT: skinny columns per pass       (t2)                           */
   int32_t cols_per_stage;  /* KC: columns per pipeline stage                                   */

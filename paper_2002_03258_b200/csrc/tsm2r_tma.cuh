@@ -227,6 +227,7 @@ struct FmaConsumer {
   using V = typename Vec<T>::type;
   static constexpr int RPT = Cfg::RPT;
   static constexpr bool kFragB = false;
+  static constexpr bool kPipelined = false;
   T acc[RPT][NT];
   int ct;
   __device__ __forceinline__ void init(int consumer_thread) {
@@ -279,6 +280,7 @@ struct Ffma2Consumer {
   using Cfg = TmaCfg<float, NT>;
   static constexpr int RPT = Cfg::RPT;
   static constexpr bool kFragB = false;
+  static constexpr bool kPipelined = false;
   static_assert(NT % 2 == 0, "pairs of columns");
   unsigned long long acc[RPT][NT / 2];  // packed (col 2p, col 2p+1)
   int ct;
@@ -329,10 +331,11 @@ struct Ffma2Consumer {
 // so each B fragment is one LDS.64 per lane. 32 DMMAs per warp per stage replace 256 DFMAs and
 // 64 LDS.128 of the FMA consumer; the FP64 datapath is shared (measured), so this buys issue
 // slots and power, not peak.
-template <int NT, int CW_ = 8>
+template <int NT, int CW_ = 8, bool PIPE_ = false>
 struct DmmaConsumer {
   using Cfg = TmaCfg<double, NT, 16 / CW_, CW_>;  // R = 512 rows for CW_ in {8, 16}
   static constexpr bool kFragB = true;
+  static constexpr bool kPipelined = PIPE_;  // k-step software pipeline (kernel loop below)
   static_assert(NT == 8 || NT == 16, "DMMA consumer needs NT in {8, 16}");
   static_assert(CW_ == 8 || CW_ == 16, "DMMA consumer: 8 or 16 consumer warps");
   static constexpr int NTI = NT / 8;       // N tiles
@@ -357,6 +360,32 @@ struct DmmaConsumer {
   // LDS.128 (rows 2g, 2g+1 of column t) feeding the even- and odd-row M tiles. (A variant that
   // loaded a whole stage's fragments first — and a look-ahead loop loading stage s+1 before stage
   // s's DMMAs — spilled at n=16 and was slower under the power cap: profiles/envab_r01.json.)
+  // One k-step's fragments (4 columns): the pipelined loop holds two of these, loading k-step j+1
+  // while the DMMAs of k-step j issue, so the LDS latency hides behind the tensor pipe.
+  static constexpr int KS = Cfg::KC / 4;
+  struct Frag {
+    double b[NTI];
+    double2 av[Q];
+  };
+  __device__ __forceinline__ void load_ks(const double* sA, const double* sB, int ks, Frag& f) const {
+    const int g = lane >> 2, t = lane & 3;
+    const double* As = sA + (RW * warp / Cfg::BOX) * (Cfg::BOX * Cfg::KC) + (RW * warp % Cfg::BOX + 2 * g);
+#pragma unroll
+    for (int nt = 0; nt < NTI; ++nt) f.b[nt] = sB[(ks * NTI + nt) * 32 + lane];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) f.av[q] = *reinterpret_cast<const double2*>(As + (4 * ks + t) * Cfg::BOX + 16 * q);
+  }
+  __device__ __forceinline__ void mma_ks(const Frag& f) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt) {
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(acc[q][0][nt][0]), "+d"(acc[q][0][nt][1]) : "d"(f.av[q].x), "d"(f.b[nt]));
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(acc[q][1][nt][0]), "+d"(acc[q][1][nt][1]) : "d"(f.av[q].y), "d"(f.b[nt]));
+      }
+  }
   __device__ __forceinline__ void stage(const double* sA, const double* sB) {
     const int g = lane >> 2, t = lane & 3;
     // the warp's rows start at RW * warp: TMA box (RW * warp) / 256, offset (RW * warp) % 256
@@ -478,6 +507,7 @@ template <typename T, int NT, int RPT_ = Vec<T>::N, int CW_ = 8>
 struct NullConsumer {
   using Cfg = TmaCfg<T, NT, RPT_, CW_>;
   static constexpr bool kFragB = false;
+  static constexpr bool kPipelined = false;
   T sink;
   int ct;
   __device__ __forceinline__ void init(int consumer_thread) {
@@ -566,6 +596,60 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
   Consumer cons;
   cons.init(threadIdx.x - 32);
   int64_t cur = -1, cur_rb = 0;
+  if constexpr (Consumer::kPipelined) {
+    // k-step software pipeline (KS = 2 k-steps of 4 columns per stage): while the DMMAs of one
+    // k-step issue, the fragments of the next are already loaded; stage s is released as soon as
+    // its last fragments are in registers, and the wait for stage s+1 happens with stage s's
+    // first-half DMMAs already in the tensor pipe.
+    static_assert(Consumer::KS == 2, "pipelined loop assumes two k-steps per stage");
+    typename Consumer::Frag f0, f1;
+    mbar_wait(&full[0], 0u);
+    int left;
+    {
+      const longlong2 md = meta[0];
+      if (md.y < 0) return;  // this CTA got no item
+      cur = md.y;
+      cur_rb = md.x & 0xffffffffll;
+      left = (int)(md.x >> 32) - 1;
+    }
+    int s = 0;
+    cons.load_ks(sA, sB, 0, f0);
+    for (int it = 1;; ++it) {
+      const T* sa = sA + (size_t)s * Cfg::A_ELEMS;
+      const T* sb = sB + (size_t)s * (Cfg::B_BYTES_PAD / sizeof(T));
+      cons.load_ks(sa, sb, 1, f1);  // last fragments of stage s: release it
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      cons.mma_ks(f0);
+      const int s1 = it % STAGES;
+      mbar_wait(&full[s1], (uint32_t)(it / STAGES) & 1u);
+      bool end = false, sw = false;
+      int64_t nxt = 0, nxt_rb = 0;
+      if (left == 0) {
+        const longlong2 md = meta[s1];
+        end = md.y < 0;
+        sw = !end;
+        nxt = md.y;
+        nxt_rb = md.x & 0xffffffffll;
+        left = (int)(md.x >> 32);
+      }
+      if (!end) cons.load_ks(sA + (size_t)s1 * Cfg::A_ELEMS, sB + (size_t)s1 * (Cfg::B_BYTES_PAD / sizeof(T)), 0, f0);
+      cons.mma_ks(f1);
+      if (end) {
+        cons.finish(a, cur_rb, cur);
+        break;
+      }
+      if (sw) {
+        cons.finish(a, cur_rb, cur);
+        cons.zero();
+        cur = nxt;
+        cur_rb = nxt_rb;
+      }
+      --left;
+      s = s1;
+    }
+    return;
+  }
   int left = 0;  // stages of the current item still to come: meta is read once per item (an LDS
                  // per stage queued behind the fragment loads of all warps cost ~15 % of issue)
   KDIAG(unsigned long long c_wait = 0, c_stage = 0, c_fin = 0, n_st = 0;)

@@ -316,7 +316,7 @@ static Tuning current_tuning() {
 // issue slots and less energy per FMA than DFMA), split-precision tf32 tensor cores for fp32
 // 16-column passes, packed FFMA2 for other fp32 widths, plain FMA otherwise.
 // TSM2X_CONSUMER=fma|dmma|ffma2|tc in the environment overrides (ablation runs).
-enum ConsumerKind { kFma = 0, kDmma = 1, kFfma2 = 2, kNull = 3, kTc = 4 };
+enum ConsumerKind { kFma = 0, kDmma = 1, kFfma2 = 2, kNull = 3, kTc = 4, kDmmaP = 5 };
 
 static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
   static const int env = [] {
@@ -325,7 +325,8 @@ static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
     if (!strcmp(e, "fma")) return (int)kFma;
     if (!strcmp(e, "dmma")) return (int)kDmma;
     if (!strcmp(e, "ffma2")) return (int)kFfma2;
-    if (!strcmp(e, "tc")) return (int)kTc;  // fp32: split-precision tf32 on tcgen05 (tsm2r_tc32.cuh)
+    if (!strcmp(e, "tc")) return (int)kTc;
+    if (!strcmp(e, "dmmap")) return (int)kDmmaP;  // DMMA, k-step software-pipelined loop  // fp32: split-precision tf32 on tcgen05 (tsm2r_tc32.cuh)
     if (!strcmp(e, "null")) return (int)kNull;  // diagnostic: pipeline only, wrong results
     return -1;
   }();
@@ -335,11 +336,13 @@ static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
                                : tu.consumer == 2 ? kDmma
                                : tu.consumer == 3 ? kFfma2
                                : tu.consumer == 4 ? kTc
+                               : tu.consumer == 5 ? kDmmaP
                                                   : -1);
   const bool dmma_ok = eb == 8 && (nt == 8 || nt == 16);
   const bool ffma2_ok = eb == 4 && nt >= 2;
   if (want == kFma) return kFma;
   if (want == kDmma) return dmma_ok ? kDmma : kFma;
+  if (want == kDmmaP) return dmma_ok ? kDmmaP : kFma;
   if (want == kFfma2) return ffma2_ok ? kFfma2 : kFma;
   if (want == kTc) return eb == 4 ? kTc : (dmma_ok ? kDmma : kFma);
   // fp64 8- and 16-column passes: DMMA. At n=8 DMMA and DFMA take the same time under the 1000 W
@@ -400,6 +403,12 @@ template <int NT, int RPT, int CW>
 struct ConsumerFor<double, NT, kDmma, RPT, CW> {
   using type = typename std::conditional<((NT == 8 || NT == 16) && RPT * CW == 16 && (CW == 8 || CW == 16)),
                                          DmmaConsumer<(NT >= 8 ? NT : 8), (CW == 16 ? 16 : 8)>,
+                                         FmaConsumer<double, NT, RPT, CW>>::type;
+};
+template <int NT, int RPT, int CW>
+struct ConsumerFor<double, NT, kDmmaP, RPT, CW> {
+  using type = typename std::conditional<((NT == 8 || NT == 16) && RPT * CW == 16 && (CW == 8 || CW == 16)),
+                                         DmmaConsumer<(NT >= 8 ? NT : 8), (CW == 16 ? 16 : 8), true>,
                                          FmaConsumer<double, NT, RPT, CW>>::type;
 };
 template <typename T, int NT, int RPT, int CW>
@@ -463,7 +472,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   const size_t acc_bytes = (atomic_split && sizeof(T) == 4) ? (size_t)a.ldacc * NT * sizeof(double) : 0;
   int kind = pick_consumer_rt(sizeof(T), NT, split, tu);
   // DMMA: the 512-row geometries (8 warps x 2 rows or 16 warps x 1 row); FFMA2: the default one
-  if (kind == kDmma && !(RPT * CW == 16 && (CW == 8 || CW == 16))) kind = kFma;
+  if ((kind == kDmma || kind == kDmmaP) && !(RPT * CW == 16 && (CW == 8 || CW == 16))) kind = kFma;
   if (kind == kFfma2 && (RPT != Vec<T>::N || CW != 8)) kind = kFma;
   if (kind == kTc) kind = (sizeof(T) == 4 && RPT == Vec<T>::N && CW == 8 && NT >= 2) ? kFfma2 : kFma;  // tc path not taken
   const size_t bt_bytes = align_up((size_t)kpad * NT * sizeof(T), 256);
@@ -487,7 +496,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
     const int64_t tot = kpad * NT + (zp ? zrows * w : 0);
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, (int64_t)di.sms * 16));
     if constexpr (sizeof(T) == 8 && (NT == 8 || NT == 16)) {
-      if (kind == kDmma) {
+      if (kind == kDmma || kind == kDmmaP) {
         prep_dyn<T, NT, true, double><<<grid, 256, 0, s>>>(B, ldb, k, kpad, w, const_cast<T*>(a.Bt), zp, zld, zrows, w);
         TSM2X_TRY(check_launch("prep_dyn"));
       } else {
@@ -514,6 +523,8 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
   if (kind == kDmma)
     TSM2X_TRY((launch_tma_kernel<T, NT, kDmma, RPT, CW>(a, tmap, G, s)));
+  else if (kind == kDmmaP)
+    TSM2X_TRY((launch_tma_kernel<T, NT, kDmmaP, RPT, CW>(a, tmap, G, s)));
   else if (kind == kFfma2)
     TSM2X_TRY((launch_tma_kernel<T, NT, kFfma2, RPT, CW>(a, tmap, G, s)));
   else if (kind == kNull)

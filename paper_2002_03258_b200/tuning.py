@@ -35,8 +35,8 @@ from typing import Dict, List, Optional
 
 from . import _lib
 
-CONSUMERS = {0: "auto", 1: "fma", 2: "dmma", 3: "ffma2", 4: "tc"}  # tsm2x_tuning.consumer
-PLAN_CONSUMERS = {0: "none", 1: "fma", 2: "dmma", 3: "ffma2", 4: "null", 5: "tc"}  # tsm2x_plan.consumer
+CONSUMERS = {0: "auto", 1: "fma", 2: "dmma", 3: "ffma2", 4: "tc", 5: "dmmap"}  # tsm2x_tuning.consumer
+PLAN_CONSUMERS = {0: "none", 1: "fma", 2: "dmma", 3: "ffma2", 4: "null", 5: "tc", 6: "dmmap"}  # tsm2x_plan.consumer
 IMPLS = {v: k for k, v in _lib.IMPL.items()}
 
 # The library's built-in defaults (tsm2x.cu make_items / pick_consumer_rt), stated here for

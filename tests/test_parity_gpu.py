@@ -391,7 +391,7 @@ def test_config4_fp32_sampled():
         _check(Ch[r0:r0 + 128], ref, k, "single", what=r0)
 
 
-@pytest.mark.parametrize("consumer", ["fma", "dmma", "ffma2", "tc", "dmma/cw16", "fma/cw16"])
+@pytest.mark.parametrize("consumer", ["fma", "dmma", "ffma2", "tc", "dmmap", "dmma/cw16", "fma/cw16"])
 def test_consumer_policies_subprocess(consumer):
     """Each TMA consumer policy (TSM2X_CONSUMER override; "/cw16" = the 16-consumer-warp x 1-row
     geometry, TSM2X_CW=16 TSM2X_RPT=1) on split and single-chunk shapes."""
