@@ -439,39 +439,39 @@ struct DmmaConsumer {
       // whole row block, 16-B aligned C: the lane's two rows (2g, 2g+1) of a column are adjacent,
       // so each access is one 16-byte vector and a warp instruction covers four full 128-B lines
       // (8 row pairs x 4 columns) instead of eight half-filled sectors per column
-      double2 old[Q][NTI][2];
+      // one 16-row group at a time (its loads, then its stores): keeps the live registers to
+      // one group's C values — the whole tile's would push the n=16 kernel into spills
 #pragma unroll
-      for (int q = 0; q < Q; ++q)
+      for (int q = 0; q < Q; ++q) {
+        double2 old[NTI][2];
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int j = 8 * nt + 2 * t + e;
-            old[q][nt][e] = (read_c && j < a.w)
-                                ? __ldcg(reinterpret_cast<const double2*>(a.C + j * a.ldc + base + 16 * q))
-                                : make_double2(0.0, 0.0);
+            old[nt][e] = (read_c && j < a.w) ? __ldcg(reinterpret_cast<const double2*>(a.C + j * a.ldc + base + 16 * q))
+                                              : make_double2(0.0, 0.0);
           }
-#pragma unroll
-      for (int q = 0; q < Q; ++q)
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int j = 8 * nt + 2 * t + e;
             if (j >= a.w) continue;
-            const double2 v = make_double2(old[q][nt][e].x + acc[q][0][nt][e], old[q][nt][e].y + acc[q][1][nt][e]);
+            const double2 v = make_double2(old[nt][e].x + acc[q][0][nt][e], old[nt][e].y + acc[q][1][nt][e]);
             double2* dst = reinterpret_cast<double2*>(a.C + j * a.ldc + base + 16 * q);
             if (nch == 1)
               __stcs(dst, v);
             else
               __stcg(dst, v);
           }
+      }
       if (nch > 1) ticket_pass(a.tickets + rb, c + 1 == nch ? 0u : (unsigned)(c + 1), leader);
       return;
     }
-    double old[Q][2][NTI][2];
 #pragma unroll
-    for (int q = 0; q < Q; ++q)
+    for (int q = 0; q < Q; ++q) {  // one 16-row group at a time (register pressure, see above)
+      double old[2][NTI][2];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -480,10 +480,8 @@ struct DmmaConsumer {
           for (int e = 0; e < 2; ++e) {
             const int64_t row = base + 16 * q + mt;
             const int j = 8 * nt + 2 * t + e;
-            old[q][mt][nt][e] = (read_c && row < a.m && j < a.w) ? __ldcg(a.C + j * a.ldc + row) : 0.0;
+            old[mt][nt][e] = (read_c && row < a.m && j < a.w) ? __ldcg(a.C + j * a.ldc + row) : 0.0;
           }
-#pragma unroll
-    for (int q = 0; q < Q; ++q)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         const int64_t row = base + 16 * q + mt;
@@ -493,9 +491,10 @@ struct DmmaConsumer {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int j = 8 * nt + 2 * t + e;
-            if (j < a.w) __stcg(a.C + j * a.ldc + row, old[q][mt][nt][e] + acc[q][mt][nt][e]);
+            if (j < a.w) __stcg(a.C + j * a.ldc + row, old[mt][nt][e] + acc[q][mt][nt][e]);
           }
       }
+    }
     if (nch > 1) ticket_pass(a.tickets + rb, c + 1 == nch ? 0u : (unsigned)(c + 1), leader);
   }
 };

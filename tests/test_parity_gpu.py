@@ -524,3 +524,33 @@ def test_tc32_nonfinite_inputs_propagate():
         assert rel_frobenius(out[fin].astype(np.float64), ref[fin]) <= 1e-5
         if det:
             assert np.array_equal(np.isnan(out), np.isnan(ref))
+
+
+def test_tsm2l_zero_c_shapes():
+    """TSM2L under the zero-C contract (L_OPT2), fp64 8/16-column passes (DMMA consumer,
+    single-chunk row blocks, 16-byte row-pair stores): ragged rows, k = 9..64, w = 9..16."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, sys
+sys.path.insert(0, ".")
+import paper_2002_03258_b200 as tsm
+from oracle import naive_gemm, rel_frobenius
+rng = np.random.default_rng(9)
+for (m, k, n) in [(1, 16, 16), (700, 16, 16), (70001, 16, 16), (5000, 9, 12), (4096, 64, 16), (513, 17, 9),
+                  (100000, 24, 16)]:
+    A = tsm.colmajor_empty(m, k, torch.float64, "cuda"); A.copy_(torch.from_numpy(rng.standard_normal((m, k))))
+    B = tsm.colmajor_empty(k, n, torch.float64, "cuda"); B.copy_(torch.from_numpy(rng.standard_normal((k, n))))
+    C = tsm.colmajor_empty(m, n, torch.float64, "cuda"); C.fill_(7.0)
+    C.zero_()
+    tsm.gemm(A, B, C, variant="l-opt2", c_is_zero=True)
+    ref = naive_gemm(A.cpu().numpy(), B.cpu().numpy(), np.zeros((m, n)))
+    err = rel_frobenius(C.cpu().numpy(), ref)
+    assert err <= 1e-12, (m, k, n, err)
+print("ok")
+'''
+    env = dict(os.environ)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr

@@ -42,8 +42,15 @@ def child(cfg, reps):
     C = tsm.colmajor_empty(m, n, dt, "cuda")
     C.zero_()
     variant = "l-opt2" if czero else "v3"
+    if os.environ.get("ENVAB_COPY"):  # reference: a plain device copy of A's bytes (read + write)
+        D = torch.empty_like(A)
+
+        def call(*_a, **_k):
+            D.copy_(A)
+    else:
+        call = tsm.gemm
     for _ in range(30):
-        tsm.gemm(A, B, C, variant=variant, c_is_zero=czero)
+        call(A, B, C, variant=variant, c_is_zero=czero)
     torch.cuda.synchronize()
     pynvml.nvmlInit()
     h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
@@ -73,7 +80,7 @@ def child(cfg, reps):
     for i in range(reps):
         if i == reps // 2:
             e1.record()
-        tsm.gemm(A, B, C, variant=variant, c_is_zero=czero)
+        call(A, B, C, variant=variant, c_is_zero=czero)
     e2.record()
     torch.cuda.synchronize()
     stop.set()
