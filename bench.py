@@ -69,7 +69,9 @@ def kernel_name(prec, m, k, n, c_is_zero):
     if p["consumer"] == "tc":
         return ("tsm2r_stream_tc32 (tcgen05 kind::tf32, split precision A.[B|lo B] + lo(A).B, accumulators in TMEM; "
                 "dynamic items)")
-    return f"tsm2r_stream_tma ({p['consumer']} consumer; dynamic items" + \
+    names = {"dmma": "DMMA m8n8k4", "dmmap": "DMMA m8n8k4, k-step software pipeline", "fma": "DFMA/FFMA",
+             "ffma2": "packed FFMA2"}
+    return f"tsm2r_stream_tma ({names.get(p['consumer'], p['consumer'])} consumer; dynamic items" + \
         ("; single-chunk row blocks)" if p["nbig"] == 0 else ")")
 
 

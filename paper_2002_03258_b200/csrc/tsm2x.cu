@@ -347,8 +347,10 @@ static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
   if (want == kTc) return eb == 4 ? kTc : (dmma_ok ? kDmma : kFma);
   // fp64 8- and 16-column passes: DMMA. At n=8 DMMA and DFMA take the same time under the 1000 W
   // cap on most parts (DMMA runs ~300 MHz higher for the same energy) and DMMA is up to 3 %
-  // faster on others (profiles/envab_r01.json); at n=16 DMMA wins outright
-  if (dmma_ok) return kDmma;
+  // faster on others (profiles/envab_r01.json); at n=16 DMMA wins outright. Split row blocks
+  // (TSM2R) use the k-step software-pipelined loop (-4.8 % n=16, -1.1 % n=8 sustained);
+  // single-chunk row blocks (TSM2L, two stages per item) the plain loop (pipelining +25 %)
+  if (dmma_ok) return split ? kDmmaP : kDmma;
   // fp32 16-column passes: split-precision tf32 on the tensor cores (tsm2r_tc32.cuh; taken when
   // the layout allows, else FFMA2): -13 % burst, -13 % sustained vs FFMA2 (profiles/envab_r01.json)
   if (eb == 4 && nt == 16) return kTc;

@@ -8,7 +8,7 @@ from paper_2002_03258_b200 import tuning
 
 def test_plan_config2_tsm2r():
     p = tuning.plan("double", 30720, 30720, 8)
-    assert p["impl"] == "tma" and p["consumer"] == "dmma"  # fp64 8-column passes (envab_r01.json)
+    assert p["impl"] == "tma" and p["consumer"] == "dmmap"  # fp64 8-column passes, pipelined (envab_r01.json)
     assert p["t1"] == 512 and p["t2"] == 8 and p["t3"] == 48
     assert p["grid"] <= 148 and p["items"] >= 24 * p["grid"] // 2
     assert p["nbig"] > 0 and p["nsmall"] > 0 and p["batch"] == 1
