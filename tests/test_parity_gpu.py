@@ -554,3 +554,36 @@ print("ok")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
+
+
+def test_cuda_graph_capture_and_replay():
+    """The device API is stream-ordered and capture-safe: tsm.gemm captured into a CUDA graph
+    (workspace from the stream-ordered allocator, work queue reset by the kernel itself) replays
+    to the same result, for TSM2R fp64 (split row blocks, fp64 reductions), fp32 on the tensor
+    cores, and TSM2L."""
+    import torch
+    tsm = _tsm()
+    rng = np.random.default_rng(21)
+    for (m, k, n, dt, variant) in [(4096, 4096, 8, torch.float64, "v3"), (4096, 3000, 16, torch.float32, "v3"),
+                                   (70000, 16, 16, torch.float64, "l-opt2")]:
+        A = tsm.colmajor_empty(m, k, dt, "cuda")
+        A.copy_(torch.from_numpy(rng.random((m, k))).to(dt))
+        B = tsm.colmajor_empty(k, n, dt, "cuda")
+        B.copy_(torch.from_numpy(rng.random((k, n))).to(dt))
+        C = tsm.colmajor_empty(m, n, dt, "cuda")
+        C.zero_()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):  # warm-up on the capture stream: its workspace exists before capture
+            tsm.gemm(A, B, C, variant=variant, c_is_zero=True)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            tsm.gemm(A, B, C, variant=variant, c_is_zero=True)
+        ref = naive_gemm(A.cpu().numpy(), B.cpu().numpy(), np.zeros((m, n), A.cpu().numpy().dtype))
+        for _ in range(3):
+            C.fill_(123.0)
+            g.replay()
+            torch.cuda.synchronize()
+            prec = "double" if dt == torch.float64 else "single"
+            assert rel_frobenius(C.cpu().numpy(), ref) <= TOL_FROB[prec], (m, k, n, dt)
