@@ -136,6 +136,20 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// L2 policy for the streamed A (TSM2X_L2POL experiments): 0 evict_first (default),
+// 1 evict_normal, 2 evict_unchanged, 3 evict_last
+__device__ __forceinline__ uint64_t policy_for(int which) {
+  uint64_t p;
+  if (which == 1)
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  else if (which == 2)
+    asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
+  else if (which == 3)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
 // Programmatic dependent launch (griddepcontrol): see prep_dyn / tsm2r_stream_tma.
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }

@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
   if (warp == 0) {
     // ---------------- producer: same queue, item order and stage tagging as tsm2r_stream_tma
     if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
+      const uint64_t pol = policy_for(a.l2pol);
       int it = 0;
       for (;;) {
         const int64_t first = (int64_t)atomicAdd(a.queue, (unsigned long long)a.it.batch);

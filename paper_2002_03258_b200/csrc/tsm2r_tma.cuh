@@ -110,6 +110,7 @@ struct DynArgs {
   unsigned* tickets;  // [num_rb] next chunk allowed to update the row block; zero between launches
   Items it;
   unsigned long long* queue;  // [0] next item, [1] low 32 bits: producers finished
+  int l2pol = 0;                      // L2 policy of the A stream (policy_for; TSM2X_L2POL)
   int diag = 0;                       // tsm2r_stream_tc32 diagnostics (TSM2X_TC_DIAG): skip bits
   unsigned long long* dbg = nullptr;  // tsm2r_stream_tc32 diagnostics: cycle counters (or null)
 };
@@ -548,7 +549,7 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
   if (warp == 0) {
     // ---------------- producer
     if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
+      const uint64_t pol = policy_for(a.l2pol);
       int it = 0;
       for (;;) {
         const int64_t first = (int64_t)atomicAdd(a.queue, (unsigned long long)a.it.batch);

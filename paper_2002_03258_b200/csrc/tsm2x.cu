@@ -188,6 +188,24 @@ static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t
 // ------------------------------------------------------------------------------------------
 
 // ---- TMA descriptor for A (2-D: dim0 = rows, dim1 = columns; OOB elements read as zero)
+// Experiment knobs read once per process: TSM2X_L2POL (L2 policy of the A stream, policy_for) and
+// TSM2X_L2PROMO (tensor-map L2 promotion: 0, 64, 128, 256 bytes; default 256).
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+static int l2_policy() {
+  static const int v = env_int("TSM2X_L2POL", 0);
+  return v;
+}
+static CUtensorMapL2promotion l2_promotion() {
+  static const int v = env_int("TSM2X_L2PROMO", 256);
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+         : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+         : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                    : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 static int encode_a_map(CUtensorMap* map, const void* A, int64_t m, int64_t k, int64_t lda, size_t eb, int box_rows,
                         int box_cols) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -206,7 +224,7 @@ static int encode_a_map(CUtensorMap* map, const void* A, int64_t m, int64_t k, i
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(map, eb == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                       const_cast<void*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TSM2X_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return TSM2X_OK;
 }
@@ -231,8 +249,8 @@ static int encode_a_map_tc32(CUtensorMap* map, const float* A, int64_t m, int64_
   cuuint32_t box[3] = {32, (cuuint32_t)Tc32Cfg::KC, (cuuint32_t)(Tc32Cfg::R / 32)};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(A), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, l2_promotion(),
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TSM2X_ECUDA, "cuTensorMapEncodeTiled (tc32) failed (%d)", (int)r);
   return TSM2X_OK;
 }
@@ -463,6 +481,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   a.w = w;
   a.c_is_zero = c_is_zero ? 1 : 0;
   a.vec_c = aligned16(C) && (ldc % Vec<T>::N == 0);
+  a.l2pol = l2_policy();
   Items& it = a.it;
   int64_t G;
   make_items(di.sms, m, k, eb, Cfg::R, Cfg::KC, NT, tu, &it, &G);
@@ -576,6 +595,7 @@ static int run_tsm2r_tc32(const DevInfo& di, Workspace* ws, int64_t m, int64_t k
   a.w = w;
   a.c_is_zero = c_is_zero ? 1 : 0;
   a.vec_c = 0;
+  a.l2pol = l2_policy();
   Items& it = a.it;
   int64_t G;
   make_items(di.sms, m, k, sizeof(float), Cfg::R, Cfg::KC, 16, tu, &it, &G);
@@ -1365,7 +1385,7 @@ int tsm2x_fill_uniform(int precision, int64_t rows, int64_t cols, void* ptr, int
 int tsm2x_set_tuning(const tsm2x_tuning* t) {
   Tuning nt;
   if (t) {
-    if (t->consumer < 0 || t->consumer > 3 || t->small_kb < 0 || t->big_kb < 0 || t->tail_pct < 0 ||
+    if (t->consumer < 0 || t->consumer > 5 || t->small_kb < 0 || t->big_kb < 0 || t->tail_pct < 0 ||
         t->tail_pct > 100 || t->batch_kb < 0 || t->combine < 0 || t->combine > 3)
       return fail(TSM2X_EINVAL, "bad tuning values");
     nt.combine = t->combine;

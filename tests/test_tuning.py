@@ -58,3 +58,15 @@ def test_tuning_knobs_round_trip_and_change_the_plan():
         tuning.set_tuning(None)
     assert tuning.get_tuning() == tuning.Tuning()
     assert tuning.plan("double", 30720, 30720, 8) == base
+
+
+def test_all_consumer_knobs_accepted():
+    for c in range(6):
+        try:
+            tuning.set_tuning(tuning.Tuning(consumer=c))
+            assert tuning.get_tuning().consumer == c
+        finally:
+            tuning.set_tuning(None)
+    with pytest.raises(ValueError):
+        tuning.set_tuning(tuning.Tuning(consumer=6))
+    tuning.set_tuning(None)

@@ -17,7 +17,10 @@ def main():
               ("tsm2r_fp64_n2", 30720, 30720, 2, "double"), ("tsm2r_fp32_n16", 32768, 32768, 16, "single"),
               ("tsm2r_fp64_n8_4096", 4096, 4096, 8, "double")]
     for name, m, k, n, prec in shapes:
-        r = tuning.tune_tsm2r(m, k, n, prec, reps=7, consumers=(0, 1, 2, 3), small_kbs=(0, 128, 1024),
+        # consumers: auto, FMA and the precision's specialised datapaths (fp64: DMMA, pipelined
+        # DMMA; fp32: FFMA2, tcgen05 split tf32)
+        cons = (0, 1, 2, 5) if prec == "double" else (0, 1, 3, 4)
+        r = tuning.tune_tsm2r(m, k, n, prec, reps=7, consumers=cons, small_kbs=(0, 128, 1024),
                               big_kbs=(0, 1024, 8192), tail_pcts=(0, 10, 35))
         out[name] = {"best": r.best.__dict__, "best_ms": r.best_ms, "default_ms": r.default_ms,
                      "top5": sorted(r.table, key=lambda x: x["ms"])[:5], "points": len(r.table)}
