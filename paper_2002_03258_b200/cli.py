@@ -36,12 +36,16 @@ B200_SPEC = {
     "num_sms": 148,
     "core_clock_max_mhz": 1965,
     "mem_bandwidth_read_gbs": 7300.0,      # read-only stream
-    "mem_bandwidth_copy_gbs": 6550.0,      # MEASURED_PEAKS.json (driver)
+    "mem_bandwidth_copy_gbs": 6550.0,      # device copy (MEASURED_PEAKS.json of an earlier box;
+                                           # 6490-6540 sustained under the cap, energy_r01.log)
     "peak_gflops_double": 36400.0,         # DFMA; DMMA m8n8k4 37100 on the same datapath
     "peak_gflops_single": 71100.0,         # FFMA; FFMA2 73000
     "shared_per_sm": 233472,
     "l2_bytes": 132644864,
-    "h2d_gbs": 55.6,
+    "h2d_gbs": 55.6,                       # 1-4 concurrent copy streams alike (tools/h2d_probe.py)
+    "power_limit_w": 1000.0,               # every sustained workload runs at this cap
+    "energy_pj_per_flop": {"dmma": 8.2, "dfma": 11.5, "ffma2": 2.6, "tcgen05_split_tf32": 3.5},
+    "pipeline_nj_per_byte": 0.135,         # TMA stream with no arithmetic, at the cap (energy_r01.log)
 }
 
 
