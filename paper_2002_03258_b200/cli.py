@@ -180,12 +180,31 @@ def cmd_tune(prec: Precision, shape, out, reps=7) -> int:
 
 
 MODEL_HEADER = ["gpu", "precision", "ridge_n", "mem_bandwidth_gbs", "peak_gflops", "m", "k", "n", "bytes",
-                "flops", "time_mem_ms", "time_comp_ms", "bound_class"]
+                "flops", "time_mem_ms", "time_comp_ms", "bound_class", "consumer", "time_power_ms",
+                "predicted_sustained_ms"]
+
+
+def _consumer_for(prec: Precision, n: int) -> str:
+    """The datapath the library picks for one pass of width n (tsm2x.cu pick_consumer_rt)."""
+    nt = 1 if n <= 1 else 2 if n <= 2 else 4 if n <= 4 else 8 if n <= 8 else 16
+    if prec is Precision.DOUBLE:
+        return "dmma" if nt >= 8 else "dfma"
+    return "tcgen05_split_tf32" if nt == 16 else "ffma2"
+
+
+def power_bound_ms(prec: Precision, m: int, k: int, n: int) -> float:
+    """Sustained time under the board power cap (DESIGN.md §4 energy model): the A stream's
+    pipeline energy plus the arithmetic's, divided by the cap."""
+    eb = prec.bytes_per_element
+    e = B200_SPEC["pipeline_nj_per_byte"] * 1e-9 * eb * m * k + \
+        B200_SPEC["energy_pj_per_flop"][_consumer_for(prec, n)] * 1e-12 * 2.0 * m * k * n
+    return e / B200_SPEC["power_limit_w"] * 1e3
 
 
 def cmd_model(prec: Precision, out) -> int:
     """B200 roofline per n at the 30720^2 problem (the reference's model table, cli.py:234-253),
-    with the corrected 2-flops-per-FMA ridge and measured peaks."""
+    with the corrected 2-flops-per-FMA ridge and measured peaks, plus the
+    power-cap bound that sets the sustained rate on this part."""
     eb = prec.bytes_per_element
     bw = B200_SPEC["mem_bandwidth_read_gbs"] * 1e9
     pk = (B200_SPEC["peak_gflops_double"] if prec is Precision.DOUBLE else B200_SPEC["peak_gflops_single"]) * 1e9
@@ -196,8 +215,13 @@ def cmd_model(prec: Precision, out) -> int:
         byts = eb * (mk * mk + mk * n + 2 * mk * n)
         flops = 2.0 * mk * mk * n
         tm, tc = byts / bw, flops / pk
+        tp = power_bound_ms(prec, mk, mk, n) / 1e3
+        # n > 16 runs ceil(n/16) passes, each re-reading A
+        passes = (n + 15) // 16
+        tp = tp if passes == 1 else passes * power_bound_ms(prec, mk, mk, 16) / 1e3
         rows.append(["B200", prec.value, ridge, bw / 1e9, pk / 1e9, mk, mk, n, byts, flops, tm * 1e3, tc * 1e3,
-                     "memory" if tm >= tc else "compute"])
+                     "memory" if tm >= tc else "compute", _consumer_for(prec, min(n, 16)), tp * 1e3,
+                     max(tm, tc, tp) * 1e3])
     _write_csv(out, MODEL_HEADER, rows)
     return 0
 

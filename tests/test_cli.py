@@ -23,6 +23,10 @@ def test_model_table(tmp_path):
     assert bounds[2] == bounds[8] == bounds[16] == "memory"  # every BASELINE config is HBM-bound
     ridge = float(rows[1][2])
     assert 16 < ridge < 24
+    # the power-cap bound: above the memory bound, growing with n
+    pred = [float(r[15]) for r in rows[1:]]
+    assert all(float(r[15]) >= float(r[10]) for r in rows[1:]) and pred == sorted(pred)
+    assert rows[3][13] == "dmma" and rows[1][13] == "dfma"
     assert open(out, "rb").read().count(b"\r") == 0
 
 
