@@ -391,7 +391,9 @@ static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, 
       tu.big_kb > 0 ? std::max(small_b, tu.big_kb * 1024.0) : std::min(4.0 * 1024 * 1024, std::max(small_b, per_cta / 6));
   const int64_t ksmall = std::max<int64_t>(KC, (int64_t)align_up((size_t)(small_b / col_bytes), KC));
   const int64_t kbig = std::max<int64_t>(ksmall, (int64_t)align_up((size_t)(big_b / col_bytes), KC));
-  const double batch_b = tu.batch_kb > 0 ? tu.batch_kb * 1024.0 : 256.0 * 1024;  // abtest_r01d.json
+  // single-chunk dispatch batch: 64 KB (one row block at k=16) — burst sweep (tuning_r01.json) and
+  // sustained A/B (-0.5 %) agree on it with the current kernel; 256 KB was the earlier choice
+  const double batch_b = tu.batch_kb > 0 ? tu.batch_kb * 1024.0 : 64.0 * 1024;
   if ((double)k * col_bytes <= 1024.0 * 1024 || k <= ksmall) {
     // single-chunk row blocks (TSM2L shapes): no split, batched dispatch
     it->nbig = 0;

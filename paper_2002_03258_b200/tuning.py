@@ -49,7 +49,7 @@ B200_DEFAULTS = {
     "small_kb": "min(512 (1024 for 16-column passes), max(64, per-CTA share / 48))",
     "big_kb": "min(4096, max(small, per-CTA share / 6))",
     "tail_pct": "20 (10 for 16-column passes)",
-    "batch_kb": 1024,
+    "batch_kb": 64,
     "combine": "fp64 atomics; deterministic=True -> chunk-ordered through per-row-block tickets (bitwise "
                "reproducible, 5-30 % slower); 3 = static stream-K split",
 }

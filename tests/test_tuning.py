@@ -19,7 +19,8 @@ def test_plan_config2_tsm2r():
 def test_plan_tsm2l_single_chunk():
     p = tuning.plan("double", 1 << 24, 16, 16)
     assert p["impl"] == "tma" and p["consumer"] == "dmma"  # fp64 16-column passes (abtest_r01e.json)
-    assert p["nbig"] == 0 and p["nsmall"] == 1 and p["batch"] > 1
+    assert p["nbig"] == 0 and p["nsmall"] == 1 and p["batch"] == 1  # 64 KB grabs = one 512x16 row block
+    assert tuning.plan("double", 1 << 24, 4, 16)["batch"] == 4
     assert tuning.plan("double", 1 << 24, 16, 8)["consumer"] == "dmma"
     assert tuning.plan("double", 1 << 24, 16, 4)["consumer"] == "fma"
 

@@ -42,6 +42,10 @@ def child(cfg, reps):
     C = tsm.colmajor_empty(m, n, dt, "cuda")
     C.zero_()
     variant = "l-opt2" if czero else "v3"
+    if os.environ.get("ENVAB_TUNING"):  # e.g. small_kb=1024:tail_pct=10 (paper_2002_03258_b200.tuning)
+        from paper_2002_03258_b200 import tuning
+        kw = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in os.environ["ENVAB_TUNING"].split(":")}
+        tuning.set_tuning(tuning.Tuning(**kw))
     if os.environ.get("ENVAB_COPY"):  # reference: a plain device copy of A's bytes (read + write)
         D = torch.empty_like(A)
 
@@ -117,7 +121,7 @@ def main():
             env = dict(os.environ)
             if c != "base":
                 for kv in c.split(","):
-                    kk, vv = kv.split("=")
+                    kk, vv = kv.split("=", 1)
                     env[kk] = vv
             p = subprocess.run([sys.executable, __file__, "--child", "--cfg", args.cfg, "--reps", str(args.reps)],
                                env=env, capture_output=True, text=True, timeout=600)
