@@ -1,4 +1,4 @@
-"""Interleaved A/B timing of tuning candidates (sustained, alternating blocks so power/clock
+"""Interleaved A/B timing of tuning candidates in one process (sustained, alternating blocks so power/clock
 drift hits every candidate alike). Usage: python tools/abtest.py [rounds]"""
 
 import json
@@ -59,7 +59,7 @@ def main():
         print(json.dumps({name: rows}), flush=True)
         del A, B, C
         torch.cuda.empty_cache()
-    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "abtest_r01.json")
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out", "abtest.json")
     with open(path, "w") as fh:
         json.dump(out, fh, indent=1)
 
