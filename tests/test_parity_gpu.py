@@ -247,11 +247,13 @@ def test_wide_n_multi_pass():
     """n > 16 runs as 16-wide passes (A re-read per pass, as the paper's t2 passes)."""
     tsm = _tsm()
     rng = np.random.default_rng(3)
-    for (m, k, n) in [(700, 300, 40), (3000, 40, 33)]:
-        A, B, C0 = rng.random((m, k)), rng.random((k, n)), rng.random((m, n))
-        out = tsm.run_native(tsm.Variant.V3, tsm.Matrix.from_2d(A, "double"), tsm.Matrix.from_2d(B, "double"),
-                             tsm.Matrix.from_2d(C0, "double"), tsm.KernelParams(t2=4))
-        _check(out.to_2d(), naive_gemm(A, B, C0), k, "double")
+    for (m, k, n) in [(700, 300, 40), (3000, 40, 33), (5000, 2000, 20)]:
+        for prec, dt in (("double", np.float64), ("single", np.float32)):
+            # fp32: 16-column passes on the tensor cores, the remainder pass on FFMA2
+            A, B, C0 = (rng.random((m, k)).astype(dt), rng.random((k, n)).astype(dt), rng.random((m, n)).astype(dt))
+            out = tsm.run_native(tsm.Variant.V3, tsm.Matrix.from_2d(A, prec), tsm.Matrix.from_2d(B, prec),
+                                 tsm.Matrix.from_2d(C0, prec), tsm.KernelParams(t2=4))
+            _check(out.to_2d(), naive_gemm(A, B, C0), k, prec, what=(m, k, n, prec))
 
 
 def test_host_path_pinned_and_pageable_slabs():
