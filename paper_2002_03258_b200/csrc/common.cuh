@@ -116,6 +116,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 #endif
 }
+// Wait with a short sleep between polls: fewer issue slots (and watts) spent by warps that
+// mostly wait — the tensor-core fp32 kernel, whose converter / MMA warps idle behind the tensor
+// pipe, is 2 % faster sustained with it; the DMMA kernels are indifferent (profiles/README.md).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, unsigned ns = 64) {
+  while (!mbar_try_wait(bar, parity)) __nanosleep(ns);
+}
 // global -> shared bulk copy completing on an mbarrier; bytes % 16 == 0, both addresses 16B-aligned.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

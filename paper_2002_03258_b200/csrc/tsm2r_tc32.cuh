@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
           for (int64_t col = col0; col < col1; col += KC, ++it) {
             const int s = it % STAGES;
             const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
-            mbar_wait(&empty[s], ph ^ 1u);
+            mbar_wait_sleep(&empty[s], ph ^ 1u);
             meta[s] = make_longlong2(rb | (nst << 32), item);  // read by the consumers once per item
             mbar_arrive_expect_tx(&full[s], tx);
             tma_load_3d(sA + (size_t)s * Cfg::A_BYTES, &tmA, 0, (int)col, (int)(rb * (R / 32)), &full[s], pol);
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
         }
       }
       const int s = it % STAGES;
-      mbar_wait(&empty[s], ((uint32_t)(it / STAGES) & 1u) ^ 1u);
+      mbar_wait_sleep(&empty[s], ((uint32_t)(it / STAGES) & 1u) ^ 1u);
       meta[s] = make_longlong2(-1, -1);
       mbar_arrive(&full[s]);
       __threadfence();
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
     for (int it = 0;; ++it) {
       const int s = it % STAGES;
       TC32_DIAG(const unsigned long long t0c = clock64();)
-      mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
+      mbar_wait_sleep(&full[s], (uint32_t)(it / STAGES) & 1u);
       TC32_DIAG(const unsigned long long t1c = clock64(); c_full += t1c - t0c;)
       if (left == 0 || sin == Cfg::SEG) {
         // new item, or SEG stages into the current segment: close the segment (its accumulators
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
         ++seg;
         sin = 0;
         TC32_DIAG(const unsigned long long ta = clock64();)
-        mbar_wait(&acc_empty[seg & 1], ((uint32_t)(seg >> 1) & 1u) ^ 1u);
+        mbar_wait_sleep(&acc_empty[seg & 1], ((uint32_t)(seg >> 1) & 1u) ^ 1u);
         TC32_DIAG(c_acc += clock64() - ta;)
         acc0 = 0;
       }
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
       --left;
       const int slot = it % Cfg::LO_SLOTS;
       TC32_DIAG(const unsigned long long t2c = clock64();)
-      mbar_wait(&lo_full[slot], (uint32_t)(it / Cfg::LO_SLOTS) & 1u);
+      mbar_wait_sleep(&lo_full[slot], (uint32_t)(it / Cfg::LO_SLOTS) & 1u);
       TC32_DIAG(const unsigned long long t3c = clock64(); c_lo += t3c - t2c;)
       tc_fence_after();
       if (elect_one()) {
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
     TC32_DIAG(unsigned long long c_full = 0, c_loe = 0, c_conv = 0, c_epi = 0;)
     // fold segment g's accumulators (buffer g & 1) into the fp64 sums and hand the buffer back
     auto drain = [&](int g) {
-      mbar_wait(&acc_full[g & 1], (uint32_t)(g >> 1) & 1u);
+      mbar_wait_sleep(&acc_full[g & 1], (uint32_t)(g >> 1) & 1u);
       tc_fence_after();
 #pragma unroll
       for (int tt = 0; tt < 2; ++tt) {
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
     for (int it = 0;; ++it) {
       const int s = it % STAGES;
       TC32_DIAG(const unsigned long long t0c = clock64();)
-      mbar_wait(&full[s], (uint32_t)(it / STAGES) & 1u);
+      mbar_wait_sleep(&full[s], (uint32_t)(it / STAGES) & 1u);
       TC32_DIAG(const unsigned long long t1c = clock64(); c_full += t1c - t0c;)
       if (left == 0) {
         const longlong2 md = meta[s];
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
       TC32_DIAG(const unsigned long long t2c = clock64();)
       if (it >= Cfg::LO_SLOTS) {  // the slot's previous stage (it - LO_SLOTS) has finished its MMAs
         const int pj = it - Cfg::LO_SLOTS;
-        mbar_wait(&empty[pj % STAGES], (uint32_t)(pj / STAGES) & 1u);
+        mbar_wait_sleep(&empty[pj % STAGES], (uint32_t)(pj / STAGES) & 1u);
       }
       TC32_DIAG(const unsigned long long t3c = clock64(); c_loe += t3c - t2c;)
       tc_fence_after();
