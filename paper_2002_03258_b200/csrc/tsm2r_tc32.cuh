@@ -202,13 +202,27 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_wait();  // Bcat and the zeroed accumulation target come from the prep kernel
+  // Programmatic dependent launch as in tsm2r_stream_tma: the producer fills the ring with A
+  // before waiting for the prep kernel (Bcat, zeroed accumulator); the other warps wait at once.
 
   if (warp == 0) {
     // ---------------- producer: same queue, item order and stage tagging as tsm2r_stream_tma
     if (lane == 0) {
       const uint64_t pol = policy_for(a.l2pol);
       int it = 0;
+      bool prep_done = false;
+      int npend = 0;
+      int pend_s[STAGES];
+      int64_t pend_col[STAGES];
+      auto flush_bt = [&]() {
+        pdl_wait();
+        prep_done = true;
+        for (int i = 0; i < npend; ++i)
+          bulk_g2s(sB + (size_t)pend_s[i] * Cfg::B_BYTES,
+                   reinterpret_cast<const unsigned char*>(a.Bt) + (pend_col[i] / KC) * Cfg::B_BYTES, Cfg::B_BYTES,
+                   &full[pend_s[i]]);
+        npend = 0;
+      };
       for (;;) {
         const int64_t first = (int64_t)atomicAdd(a.queue, (unsigned long long)a.it.batch);
         if (first >= a.it.total) break;
@@ -225,11 +239,18 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
             meta[s] = make_longlong2(rb | (nst << 32), item);  // read by the consumers once per item
             mbar_arrive_expect_tx(&full[s], tx);
             tma_load_3d(sA + (size_t)s * Cfg::A_BYTES, &tmA, 0, (int)col, (int)(rb * (R / 32)), &full[s], pol);
-            bulk_g2s(sB + (size_t)s * Cfg::B_BYTES, reinterpret_cast<const unsigned char*>(a.Bt) + (col / KC) * Cfg::B_BYTES,
-                     Cfg::B_BYTES, &full[s]);
+            if (prep_done) {
+              bulk_g2s(sB + (size_t)s * Cfg::B_BYTES, reinterpret_cast<const unsigned char*>(a.Bt) + (col / KC) * Cfg::B_BYTES,
+                       Cfg::B_BYTES, &full[s]);
+            } else {
+              pend_s[npend] = s;
+              pend_col[npend] = col;
+              if (++npend == STAGES) flush_bt();
+            }
           }
         }
       }
+      if (!prep_done) flush_bt();
       const int s = it % STAGES;
       mbar_wait_sleep(&empty[s], ((uint32_t)(it / STAGES) & 1u) ^ 1u);
       meta[s] = make_longlong2(-1, -1);
@@ -243,6 +264,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
       }
     }
   } else if (warp == 1) {
+    pdl_wait();
     // ---------------- MMA issuer: the whole warp walks the pipeline, one elected lane issues.
     // The issue path is a single dependent instruction stream sharing its SM sub-partition with
     // two converter warps, so it is kept short: descriptors are built once per stage and the
@@ -325,6 +347,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
     })
   } else {
     // ---------------- converters + epilogue
+    pdl_wait();
     const int cw = warp - 2;        // 0..7
     const int q = warp & 3;         // TMEM lane quarter this warp may access
     const int t0 = 2 * (cw >> 2);   // tiles t0, t0 + 1

@@ -544,13 +544,28 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
   }
   __syncthreads();
-  pdl_wait();  // Bt and the zeroed accumulation target come from the prep kernel
+  // Programmatic dependent launch: Bt and the zeroed accumulation target come from the prep
+  // kernel, A does not. The producer fills the ring with A tiles first and waits for prep only
+  // before the first Bt copy is due (the stage barriers expect both); the consumers wait at once
+  // (they write C / the accumulator, which prep may have zeroed).
 
   if (warp == 0) {
     // ---------------- producer
     if (lane == 0) {
       const uint64_t pol = policy_for(a.l2pol);
       int it = 0;
+      bool prep_done = false;
+      int npend = 0;
+      int pend_s[STAGES];
+      int64_t pend_col[STAGES];
+      auto flush_bt = [&]() {  // Bt copies of the stages issued before prep completed
+        pdl_wait();
+        prep_done = true;
+        for (int i = 0; i < npend; ++i)
+          bulk_g2s(sB + (size_t)pend_s[i] * (Cfg::B_BYTES_PAD / sizeof(T)), a.Bt + pend_col[i] * NT, Cfg::B_BYTES,
+                   &full[pend_s[i]]);
+        npend = 0;
+      };
       for (;;) {
         const int64_t first = (int64_t)atomicAdd(a.queue, (unsigned long long)a.it.batch);
         if (first >= a.it.total) break;
@@ -571,10 +586,17 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
             for (int b = 0; b < nbox; ++b)
               tma_load_2d(sA + (size_t)s * Cfg::A_ELEMS + b * (Cfg::BOX * KC), &tmA, (int)(row_base + b * Cfg::BOX),
                           (int)col, &full[s], pol);
-            bulk_g2s(sB + (size_t)s * (Cfg::B_BYTES_PAD / sizeof(T)), a.Bt + col * NT, Cfg::B_BYTES, &full[s]);
+            if (prep_done) {
+              bulk_g2s(sB + (size_t)s * (Cfg::B_BYTES_PAD / sizeof(T)), a.Bt + col * NT, Cfg::B_BYTES, &full[s]);
+            } else {
+              pend_s[npend] = s;
+              pend_col[npend] = col;
+              if (++npend == STAGES) flush_bt();  // ring full: nothing more to issue before prep
+            }
           }
         }
       }
+      if (!prep_done) flush_bt();
       // end-of-work marker for the consumers
       const int s = it % STAGES;
       mbar_wait(&empty[s], ((uint32_t)(it / STAGES) & 1u) ^ 1u);
@@ -593,6 +615,7 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
   }
 
   // ---------------- consumers
+  pdl_wait();
   Consumer cons;
   cons.init(threadIdx.x - 32);
   int64_t cur = -1, cur_rb = 0;
