@@ -637,6 +637,7 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
     }
     int s = 0;
     cons.load_ks(sA, sB, 0, f0);
+    KDIAG(unsigned long long c_wait = 0, c_fin = 0, n_st = 0; const unsigned long long t_start = clock64();)
     for (int it = 1;; ++it) {
       const T* sa = sA + (size_t)s * Cfg::A_ELEMS;
       const T* sb = sB + (size_t)s * (Cfg::B_BYTES_PAD / sizeof(T));
@@ -645,7 +646,9 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
       if (lane == 0) mbar_arrive(&empty[s]);
       cons.mma_ks(f0);
       const int s1 = it % STAGES;
+      KDIAG(const unsigned long long tw0 = clock64();)
       mbar_wait(&full[s1], (uint32_t)(it / STAGES) & 1u);
+      KDIAG(c_wait += clock64() - tw0; ++n_st;)
       bool end = false, sw = false;
       int64_t nxt = 0, nxt_rb = 0;
       if (left == 0) {
@@ -663,14 +666,22 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
         break;
       }
       if (sw) {
+        KDIAG(const unsigned long long tf0 = clock64();)
         cons.finish(a, cur_rb, cur);
         cons.zero();
         cur = nxt;
         cur_rb = nxt_rb;
+        KDIAG(c_fin += clock64() - tf0;)
       }
       --left;
       s = s1;
     }
+    KDIAG(if (a.dbg && threadIdx.x == 32) {
+      atomicAdd(a.dbg + 0, c_wait);
+      atomicAdd(a.dbg + 1, clock64() - t_start);  // "stage" = whole loop time
+      atomicAdd(a.dbg + 2, c_fin);
+      atomicAdd(a.dbg + 4, n_st);
+    })
     return;
   }
   int left = 0;  // stages of the current item still to come: meta is read once per item (an LDS
