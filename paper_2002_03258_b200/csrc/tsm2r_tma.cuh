@@ -37,7 +37,7 @@
 
 namespace tsm2x {
 
-template <typename T, int NT, int RPT_ = Vec<T>::N, int CW_ = 8>
+template <typename T, int NT, int RPT_ = Vec<T>::N, int CW_ = 8, int SB_ = 32768>
 struct TmaCfg {
   static constexpr int CW = CW_;                      // consumer warps
   static constexpr int CT = 32 * CW;                  // consumer threads
@@ -46,9 +46,10 @@ struct TmaCfg {
   static constexpr int R = CT * RPT;                  // rows per row block (512 fp64 / 1024 fp32)
   static constexpr int BOX = 256;                     // rows per TMA box (box dim limit)
   static constexpr int NBOX = R / BOX;
-  static constexpr int KC = 32768 / (R * (int)sizeof(T));  // columns per 32 KB stage (8 by default)
+  static constexpr int SB = SB_;                      // A bytes per stage (32 KB; 64 KB experiment)
+  static constexpr int KC = SB / (R * (int)sizeof(T));  // columns per stage (8 by default)
   static_assert(KC >= 1 && (KC * NT * (int)sizeof(T)) % 16 == 0, "bulk-copy granularity");
-  static constexpr int STAGES = 6;
+  static constexpr int STAGES = 196608 / SB;           // 192 KB of A in the ring
   static constexpr int A_ELEMS = R * KC;
   static constexpr int B_ELEMS = KC * NT;
   static constexpr int A_BYTES = A_ELEMS * (int)sizeof(T);
@@ -222,9 +223,9 @@ __device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int
 
 // FMA: thread ct owns rows ct + 256*r; one scalar LDS per row per column (32 consecutive
 // elements per warp, conflict-free), Bt row as broadcast LDS.128s, NT FMAs per row per column.
-template <typename T, int NT, int RPT_ = Vec<T>::N, int CW_ = 8>
+template <typename T, int NT, int RPT_ = Vec<T>::N, int CW_ = 8, int SB_ = 32768>
 struct FmaConsumer {
-  using Cfg = TmaCfg<T, NT, RPT_, CW_>;
+  using Cfg = TmaCfg<T, NT, RPT_, CW_, SB_>;
   using V = typename Vec<T>::type;
   static constexpr int RPT = Cfg::RPT;
   static constexpr bool kFragB = false;
@@ -332,9 +333,9 @@ struct Ffma2Consumer {
 // so each B fragment is one LDS.64 per lane. 32 DMMAs per warp per stage replace 256 DFMAs and
 // 64 LDS.128 of the FMA consumer; the FP64 datapath is shared (measured), so this buys issue
 // slots and power, not peak.
-template <int NT, int CW_ = 8, bool PIPE_ = false>
+template <int NT, int CW_ = 8, bool PIPE_ = false, int SB_ = 32768>
 struct DmmaConsumer {
-  using Cfg = TmaCfg<double, NT, 16 / CW_, CW_>;  // R = 512 rows for CW_ in {8, 16}
+  using Cfg = TmaCfg<double, NT, 16 / CW_, CW_, SB_>;  // R = 512 rows for CW_ in {8, 16}
   static constexpr bool kFragB = true;
   static constexpr bool kPipelined = PIPE_;  // k-step software pipeline (kernel loop below)
   static_assert(NT == 8 || NT == 16, "DMMA consumer needs NT in {8, 16}");
@@ -368,15 +369,30 @@ struct DmmaConsumer {
     double b[NTI];
     double2 av[Q];
   };
+  KDIAG(int dg = 0;)  // diagnostic build: 16 = no fragment LDS (constants), 32 = no DMMA
   __device__ __forceinline__ void load_ks(const double* sA, const double* sB, int ks, Frag& f) const {
     const int g = lane >> 2, t = lane & 3;
     const double* As = sA + (RW * warp / Cfg::BOX) * (Cfg::BOX * Cfg::KC) + (RW * warp % Cfg::BOX + 2 * g);
+    KDIAG(if (dg & 16) {
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt) f.b[nt] = 1.0 + ks;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) f.av[q] = make_double2(lane + q, lane - q);
+      return;
+    })
 #pragma unroll
     for (int nt = 0; nt < NTI; ++nt) f.b[nt] = sB[(ks * NTI + nt) * 32 + lane];
 #pragma unroll
     for (int q = 0; q < Q; ++q) f.av[q] = *reinterpret_cast<const double2*>(As + (4 * ks + t) * Cfg::BOX + 16 * q);
   }
   __device__ __forceinline__ void mma_ks(const Frag& f) {
+    KDIAG(if (dg & 32) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt) acc[q][0][nt][0] += f.av[q].x + f.av[q].y + f.b[nt];
+      return;
+    })
 #pragma unroll
     for (int q = 0; q < Q; ++q)
 #pragma unroll
@@ -503,9 +519,9 @@ struct DmmaConsumer {
 // Diagnostic only (TSM2X_CONSUMER=null): touches one element per stage and writes nothing —
 // isolates the cost (time, power) of the TMA pipeline itself from the arithmetic. Results are
 // garbage by design; never selected automatically.
-template <typename T, int NT, int RPT_ = Vec<T>::N, int CW_ = 8>
+template <typename T, int NT, int RPT_ = Vec<T>::N, int CW_ = 8, int SB_ = 32768>
 struct NullConsumer {
-  using Cfg = TmaCfg<T, NT, RPT_, CW_>;
+  using Cfg = TmaCfg<T, NT, RPT_, CW_, SB_>;
   static constexpr bool kFragB = false;
   static constexpr bool kPipelined = false;
   T sink;
@@ -624,8 +640,10 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
     // k-step issue, the fragments of the next are already loaded; stage s is released as soon as
     // its last fragments are in registers, and the wait for stage s+1 happens with stage s's
     // first-half DMMAs already in the tensor pipe.
-    static_assert(Consumer::KS == 2, "pipelined loop assumes two k-steps per stage");
+    constexpr int KS = Consumer::KS;
+    static_assert(KS % 2 == 0, "pipelined loop alternates two fragment sets over an even k-step count");
     typename Consumer::Frag f0, f1;
+    KDIAG(cons.dg = a.diag;)
     mbar_wait(&full[0], 0u);
     int left;
     {
@@ -641,10 +659,27 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
     for (int it = 1;; ++it) {
       const T* sa = sA + (size_t)s * Cfg::A_ELEMS;
       const T* sb = sB + (size_t)s * (Cfg::B_BYTES_PAD / sizeof(T));
-      cons.load_ks(sa, sb, 1, f1);  // last fragments of stage s: release it
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      cons.mma_ks(f0);
+      // k-steps 0 .. KS-2 of stage s: load the next k-step, issue this one; the stage is released
+      // once its last k-step's fragments are loaded
+#pragma unroll
+      for (int ks = 0; ks < KS - 1; ++ks) {
+        if (ks % 2 == 0) {
+          cons.load_ks(sa, sb, ks + 1, f1);
+          if (ks + 1 == KS - 1) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+          }
+          cons.mma_ks(f0);
+        } else {
+          cons.load_ks(sa, sb, ks + 1, f0);
+          if (ks + 1 == KS - 1) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+          }
+          cons.mma_ks(f1);
+        }
+      }
+      // last k-step (held in f1, KS even): fetch stage s+1's first k-step into f0 meanwhile
       const int s1 = it % STAGES;
       KDIAG(const unsigned long long tw0 = clock64();)
       mbar_wait(&full[s1], (uint32_t)(it / STAGES) & 1u);

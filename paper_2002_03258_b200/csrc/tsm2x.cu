@@ -417,37 +417,38 @@ static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, 
   *grid = std::min<int64_t>(G_full, (it->total + it->batch - 1) / it->batch);
 }
 
-template <typename T, int NT, int KIND, int RPT, int CW>
+template <typename T, int NT, int KIND, int RPT, int CW, int SB = 32768>
 struct ConsumerFor {
-  using type = FmaConsumer<T, NT, RPT, CW>;
+  using type = FmaConsumer<T, NT, RPT, CW, SB>;
 };
-template <int NT, int RPT, int CW>
-struct ConsumerFor<double, NT, kDmma, RPT, CW> {
+template <int NT, int RPT, int CW, int SB>
+struct ConsumerFor<double, NT, kDmma, RPT, CW, SB> {
   using type = typename std::conditional<((NT == 8 || NT == 16) && RPT * CW == 16 && (CW == 8 || CW == 16)),
-                                         DmmaConsumer<(NT >= 8 ? NT : 8), (CW == 16 ? 16 : 8)>,
-                                         FmaConsumer<double, NT, RPT, CW>>::type;
+                                         DmmaConsumer<(NT >= 8 ? NT : 8), (CW == 16 ? 16 : 8), false, SB>,
+                                         FmaConsumer<double, NT, RPT, CW, SB>>::type;
 };
-template <int NT, int RPT, int CW>
-struct ConsumerFor<double, NT, kDmmaP, RPT, CW> {
+template <int NT, int RPT, int CW, int SB>
+struct ConsumerFor<double, NT, kDmmaP, RPT, CW, SB> {
   using type = typename std::conditional<((NT == 8 || NT == 16) && RPT * CW == 16 && (CW == 8 || CW == 16)),
-                                         DmmaConsumer<(NT >= 8 ? NT : 8), (CW == 16 ? 16 : 8), true>,
-                                         FmaConsumer<double, NT, RPT, CW>>::type;
+                                         DmmaConsumer<(NT >= 8 ? NT : 8), (CW == 16 ? 16 : 8), true, SB>,
+                                         FmaConsumer<double, NT, RPT, CW, SB>>::type;
 };
-template <typename T, int NT, int RPT, int CW>
-struct ConsumerFor<T, NT, kNull, RPT, CW> {
-  using type = NullConsumer<T, NT, RPT, CW>;
+template <typename T, int NT, int RPT, int CW, int SB>
+struct ConsumerFor<T, NT, kNull, RPT, CW, SB> {
+  using type = NullConsumer<T, NT, RPT, CW, SB>;
 };
-template <int NT, int RPT, int CW>
-struct ConsumerFor<float, NT, kFfma2, RPT, CW> {
-  using type = typename std::conditional<(NT >= 2 && RPT == 4 && CW == 8), Ffma2Consumer<(NT >= 2 ? NT : 2)>,
-                                         FmaConsumer<float, NT, RPT, CW>>::type;
+template <int NT, int RPT, int CW, int SB>
+struct ConsumerFor<float, NT, kFfma2, RPT, CW, SB> {
+  using type = typename std::conditional<(NT >= 2 && RPT == 4 && CW == 8 && SB == 32768), Ffma2Consumer<(NT >= 2 ? NT : 2)>,
+                                         FmaConsumer<float, NT, RPT, CW, SB>>::type;
 };
 
-template <typename T, int NT, int KIND, int RPT, int CW>
+template <typename T, int NT, int KIND, int RPT, int CW, int SB = 32768>
 static int launch_tma_kernel(const DynArgs<T>& a_in, const CUtensorMap& tmap_in, int64_t G, cudaStream_t s) {
-  using Cons = typename ConsumerFor<T, NT, KIND, RPT, CW>::type;
+  using Cons = typename ConsumerFor<T, NT, KIND, RPT, CW, SB>::type;
   using Cfg = typename Cons::Cfg;
-  static_assert(Cfg::R == TmaCfg<T, NT, RPT, CW>::R, "consumer / plan row-block mismatch");
+  static_assert(Cfg::R == TmaCfg<T, NT, RPT, CW, SB>::R && Cfg::KC == TmaCfg<T, NT, RPT, CW, SB>::KC,
+                "consumer / plan geometry mismatch");
   auto kern = tsm2r_stream_tma<T, NT, Cons>;
   TSM2X_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   DynArgs<T> a = a_in;
@@ -468,11 +469,11 @@ static int launch_tma_kernel(const DynArgs<T>& a_in, const CUtensorMap& tmap_in,
 }
 
 // TMA flavour, dynamic items (tsm2r_tma.cuh): item sizes from the per-CTA share of the work.
-template <typename T, int NT, int RPT = Vec<T>::N, int CW = 8>
+template <typename T, int NT, int RPT = Vec<T>::N, int CW = 8, int SB = 32768>
 static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k, int w, const T* A, int64_t lda,
                          const T* B, int64_t ldb, T* C, int64_t ldc, bool c_is_zero, bool ordered,
                          cudaStream_t s) {
-  using Cfg = TmaCfg<T, NT, RPT, CW>;
+  using Cfg = TmaCfg<T, NT, RPT, CW, SB>;
   const size_t eb = sizeof(T);
   const Tuning tu = current_tuning();
   DynArgs<T> a;
@@ -496,7 +497,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   int kind = pick_consumer_rt(sizeof(T), NT, split, tu);
   // DMMA: the 512-row geometries (8 warps x 2 rows or 16 warps x 1 row); FFMA2: the default one
   if ((kind == kDmma || kind == kDmmaP) && !(RPT * CW == 16 && (CW == 8 || CW == 16))) kind = kFma;
-  if (kind == kFfma2 && (RPT != Vec<T>::N || CW != 8)) kind = kFma;
+  if (kind == kFfma2 && (RPT != Vec<T>::N || CW != 8 || SB != 32768)) kind = kFma;
   if (kind == kTc) kind = (sizeof(T) == 4 && RPT == Vec<T>::N && CW == 8 && NT >= 2) ? kFfma2 : kFma;  // tc path not taken
   const size_t bt_bytes = align_up((size_t)kpad * NT * sizeof(T), 256);
   TSM2X_TRY(ws_reserve(ws, bt_bytes + acc_bytes, (size_t)it.num_rb + 8, s));
@@ -538,6 +539,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
     if (!dbg) TSM2X_CUDA(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
     TSM2X_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), s));
     a.dbg = dbg;
+    a.diag = atoi(getenv("TSM2X_TC_DIAG"));
   }
 #endif
   alignas(64) CUtensorMap tmap;
@@ -545,15 +547,15 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   const bool timed = t_ev_start && t_ev_stop;
   if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
   if (kind == kDmma)
-    TSM2X_TRY((launch_tma_kernel<T, NT, kDmma, RPT, CW>(a, tmap, G, s)));
+    TSM2X_TRY((launch_tma_kernel<T, NT, kDmma, RPT, CW, SB>(a, tmap, G, s)));
   else if (kind == kDmmaP)
-    TSM2X_TRY((launch_tma_kernel<T, NT, kDmmaP, RPT, CW>(a, tmap, G, s)));
+    TSM2X_TRY((launch_tma_kernel<T, NT, kDmmaP, RPT, CW, SB>(a, tmap, G, s)));
   else if (kind == kFfma2)
-    TSM2X_TRY((launch_tma_kernel<T, NT, kFfma2, RPT, CW>(a, tmap, G, s)));
+    TSM2X_TRY((launch_tma_kernel<T, NT, kFfma2, RPT, CW, SB>(a, tmap, G, s)));
   else if (kind == kNull)
-    TSM2X_TRY((launch_tma_kernel<T, NT, kNull, RPT, CW>(a, tmap, G, s)));
+    TSM2X_TRY((launch_tma_kernel<T, NT, kNull, RPT, CW, SB>(a, tmap, G, s)));
   else
-    TSM2X_TRY((launch_tma_kernel<T, NT, kFma, RPT, CW>(a, tmap, G, s)));
+    TSM2X_TRY((launch_tma_kernel<T, NT, kFma, RPT, CW, SB>(a, tmap, G, s)));
 #ifdef TSM2X_TC32_DIAG
   if (diag) {
     unsigned long long h[16];
@@ -831,7 +833,17 @@ static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m,
       const char* e = getenv("TSM2X_CW");
       return e ? atoi(e) : 0;
     }();
+    // fp64 8/16-column passes (DMMA): 64 KB stages x 3 by default — half the barrier round trips
+    // and stage hand-offs per byte for a consumer bound by fragment-load latency (sustained
+    // -0.6 % n=8, -1.2 % n=16, -1 to -3 % TSM2L; profiles/README.md); TSM2X_STAGE_KB=32 restores
+    // 32 KB x 6
+    static const int env_stage_kb = [] {
+      const char* e = getenv("TSM2X_STAGE_KB");
+      return e ? atoi(e) : 64;
+    }();
     if constexpr (sizeof(T) == 8 && (NT == 8 || NT == 16)) {
+      if (env_stage_kb == 64 && env_cw == 0 && env_rpt == 0)
+        return run_tsm2r_tma<T, NT, 2, 8, 65536>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
       if (env_cw == 16 && env_rpt == 1)  // 16 consumer warps x 1 row: 512-row blocks (DMMA-capable)
         return run_tsm2r_tma<T, NT, 1, 16>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
     }
@@ -1451,10 +1463,13 @@ int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, 
   out->impl = TSM2X_IMPL_STREAM_TMA;
   const int R = 256 * (int)(16 / eb);
   out->rows_per_block = R;
-  out->cols_per_stage = TmaCfg<double, 1>::KC;
-  out->stages = TmaCfg<double, 1>::STAGES;
+  const bool stage64 = eb == 8 && (nt == 8 || nt == 16) && getenv("TSM2X_STAGE_KB") == nullptr;
+  out->cols_per_stage = stage64 ? TmaCfg<double, 8, 2, 8, 65536>::KC : TmaCfg<double, 1>::KC;
+  out->stages = stage64 ? TmaCfg<double, 8, 2, 8, 65536>::STAGES : TmaCfg<double, 1>::STAGES;
   const Tuning tu0 = current_tuning();
   if (tu0.combine == 3) {
+    out->cols_per_stage = TmaCfg<double, 1>::KC;  // the static kernel keeps 32 KB stages
+    out->stages = TmaCfg<double, 1>::STAGES;
     out->deterministic = 1;
     out->consumer = 1;
     const int64_t units = ((m + R - 1) / R) * ((k + 7) / 8);

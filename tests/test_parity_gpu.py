@@ -393,7 +393,8 @@ def test_config4_fp32_sampled():
         _check(Ch[r0:r0 + 128], ref, k, "single", what=r0)
 
 
-@pytest.mark.parametrize("consumer", ["fma", "dmma", "ffma2", "tc", "dmmap", "dmma/cw16", "fma/cw16"])
+@pytest.mark.parametrize("consumer", ["fma", "dmma", "ffma2", "tc", "dmmap", "dmma/cw16", "fma/cw16", "auto/sb64",
+                                      "dmma/sb64"])
 def test_consumer_policies_subprocess(consumer):
     """Each TMA consumer policy (TSM2X_CONSUMER override; "/cw16" = the 16-consumer-warp x 1-row
     geometry, TSM2X_CW=16 TSM2X_RPT=1) on split and single-chunk shapes."""
@@ -419,9 +420,13 @@ for (m, k, n) in [(2000, 5000, 16), (1500, 3001, 8), (777, 10000, 12), (4096, 16
         assert err <= tol, (m, k, n, dt, err)
 print("ok")
 '''
-    env = dict(os.environ, TSM2X_CONSUMER=consumer.split("/")[0])
+    env = dict(os.environ)
+    if not consumer.startswith("auto"):
+        env["TSM2X_CONSUMER"] = consumer.split("/")[0]
     if consumer.endswith("/cw16"):
         env.update(TSM2X_CW="16", TSM2X_RPT="1")
+    if consumer.endswith("/sb64"):  # 64 KB pipeline stages (fp64 8/16-column passes)
+        env.update(TSM2X_STAGE_KB="64")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
