@@ -44,7 +44,7 @@ B200_SPEC = {
     "l2_bytes": 132644864,
     "h2d_gbs": 55.6,                       # 1-4 concurrent copy streams alike (tools/h2d_probe.py)
     "power_limit_w": 1000.0,               # every sustained workload runs at this cap
-    "energy_pj_per_flop": {"dmma": 8.2, "dfma": 11.5, "ffma2": 2.6, "tcgen05_split_tf32": 3.5},
+    "energy_pj_per_flop": {"dmma": 8.8, "dfma": 13.0, "ffma2": 3.4, "tcgen05_split_tf32": 3.5},
     "pipeline_nj_per_byte": 0.135,         # TMA stream with no arithmetic, at the cap (energy_r01.log)
 }
 
