@@ -639,7 +639,7 @@ static int run_tsm2r_tc32(const DevInfo& di, Workspace* ws, int64_t m, int64_t k
 #endif
   alignas(64) CUtensorMap tmap;
   TSM2X_TRY(encode_a_map_tc32(&tmap, A, m, k, lda));
-  auto kern = tsm2r_stream_tc32;
+  auto kern = split ? tsm2r_stream_tc32<false> : tsm2r_stream_tc32<true>;
   TSM2X_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   const bool timed = t_ev_start && t_ev_stop;
   if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
