@@ -383,12 +383,16 @@ static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, 
   it->num_rb = (m + R - 1) / R;
   const double col_bytes = (double)R * eb;  // one column of one row block
   const double per_cta = (double)m * k * eb / (double)G_full;
-  // 16-column passes: fewer, larger small items and a shorter small-item tail (fewer fp64
-  // reductions per byte; sustained A/B, profiles/abtest_r01.json)
-  const double small_cap = nt >= 16 ? 1024.0 * 1024 : 512.0 * 1024;
+  // 16-column passes and the fp64 DMMA passes: fewer, larger items and a shorter small-item
+  // tail (fewer item epilogues and fp64 reductions per byte; sustained A/B,
+  // profiles/abtest_r01.json, and for the 64 KB-stage DMMA passes small 1 MB + tail 10 % + big
+  // 8 MB: n=8 -1.6 %, big 8 MB at n=16 -0.7 %). The caps only bind for large problems.
+  const bool dmma_pass = eb == 8 && nt >= 8;
+  const double small_cap = (nt >= 16 || dmma_pass) ? 1024.0 * 1024 : 512.0 * 1024;
+  const double big_cap = dmma_pass ? 8.0 * 1024 * 1024 : 4.0 * 1024 * 1024;
   const double small_b = tu.small_kb > 0 ? tu.small_kb * 1024.0 : std::min(small_cap, std::max(64.0 * 1024, per_cta / 48));
   const double big_b =
-      tu.big_kb > 0 ? std::max(small_b, tu.big_kb * 1024.0) : std::min(4.0 * 1024 * 1024, std::max(small_b, per_cta / 6));
+      tu.big_kb > 0 ? std::max(small_b, tu.big_kb * 1024.0) : std::min(big_cap, std::max(small_b, per_cta / 6));
   const int64_t ksmall = std::max<int64_t>(KC, (int64_t)align_up((size_t)(small_b / col_bytes), KC));
   const int64_t kbig = std::max<int64_t>(ksmall, (int64_t)align_up((size_t)(big_b / col_bytes), KC));
   // single-chunk dispatch batch: 64 KB (one row block at k=16) — burst sweep (tuning_r01.json) and
@@ -403,7 +407,7 @@ static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, 
     it->ksmall = (int64_t)align_up((size_t)k, KC);
     it->batch = std::max<int64_t>(1, (int64_t)(batch_b / ((double)k * col_bytes)));
   } else {
-    const int pct = tu.tail_pct > 0 ? std::min(tu.tail_pct, 100) : (nt >= 16 ? 10 : 20);
+    const int pct = tu.tail_pct > 0 ? std::min(tu.tail_pct, 100) : ((nt >= 16 || dmma_pass) ? 10 : 20);
     const int64_t tail_cols = std::max<int64_t>(1, (k * pct + 99) / 100);
     const int64_t tail = std::min<int64_t>(k, (int64_t)align_up((size_t)tail_cols, (size_t)ksmall));
     it->kbig_end = ((k - tail) / KC) * KC;

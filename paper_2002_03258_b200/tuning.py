@@ -46,9 +46,9 @@ B200_DEFAULTS = {
                 "plain loop for single-chunk ones); split-precision tf32 on the tensor cores (tc) "
                 "for fp32 16-column passes; FFMA2 for other fp32 n >= 2; else FMA "
                 "(sustained A/B under the 1000 W cap: profiles/envab_r01.json)",
-    "small_kb": "min(512 (1024 for 16-column passes), max(64, per-CTA share / 48))",
-    "big_kb": "min(4096, max(small, per-CTA share / 6))",
-    "tail_pct": "20 (10 for 16-column passes)",
+    "small_kb": "min(512 (1024 for 16-column and fp64 DMMA passes), max(64, per-CTA share / 48))",
+    "big_kb": "min(4096 (8192 for fp64 DMMA passes), max(small, per-CTA share / 6))",
+    "tail_pct": "20 (10 for 16-column and fp64 DMMA passes)",
     "batch_kb": 64,
     "combine": "fp64 atomics; deterministic=True -> chunk-ordered through per-row-block tickets (bitwise "
                "reproducible, 5-30 % slower); 3 = static stream-K split",
