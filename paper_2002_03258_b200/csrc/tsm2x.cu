@@ -406,6 +406,33 @@ static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, 
     it->nsmall = 1;
     it->ksmall = (int64_t)align_up((size_t)k, KC);
     it->batch = std::max<int64_t>(1, (int64_t)(batch_b / ((double)k * col_bytes)));
+  } else if (tu.small_kb == 0 && tu.big_kb == 0 && tu.tail_pct == 0 && per_cta <= 4.0 * 1024 * 1024) {
+    // mid-size problems (A up to ~600 MB): about one item per CTA, equal column ranges per row
+    // block. Per-item epilogues and the ramp, not HBM, set the time here; the queue's tail
+    // balancing buys nothing (ncu, cold: 2048^2 n=16 25 -> 17 us, 4096^2 n=16 36 -> 29 us,
+    // 6144^2 n=16 69 -> 51 us, 8192^2 n=16 95 -> 83-87 us, n=8 -3 to -12 %;
+    // profiles/midsize_r01.jsonl)
+    // pieces per row block: minimise the makespan (rounds of items per CTA x item columns, plus a
+    // per-item cost of ~KC columns for the epilogue)
+    int64_t c = (int64_t)align_up((size_t)k, KC);
+    double best = 1e300;
+    for (int64_t p = 1; p <= 256; ++p) {
+      const int64_t cp = std::max<int64_t>(KC, (int64_t)align_up((size_t)((k + p - 1) / p), KC));
+      const int64_t np = (k + cp - 1) / cp;
+      const int64_t rounds = (it->num_rb * np + G_full - 1) / G_full;
+      const double cost = (double)rounds * (double)(cp + KC);
+      if (cost < best) {
+        best = cost;
+        c = cp;
+      }
+      if (cp == KC) break;
+    }
+    it->nbig = 0;
+    it->kbig = c;
+    it->kbig_end = 0;
+    it->ksmall = c;
+    it->nsmall = (k + c - 1) / c;
+    it->batch = 1;
   } else {
     const int pct = tu.tail_pct > 0 ? std::min(tu.tail_pct, 100) : ((nt >= 16 || dmma_pass) ? 10 : 20);
     const int64_t tail_cols = std::max<int64_t>(1, (k * pct + 99) / 100);

@@ -18,6 +18,25 @@ def test_plan_config2_tsm2r():
         >= 0.15 * 30720  # DFMA passes keep the 20 % tail
 
 
+@pytest.mark.parametrize("mk,n,prec", [(2048, 16, "double"), (4096, 8, "double"), (6144, 16, "double"),
+                                       (8192, 8, "double"), (4096, 16, "single")])
+def test_plan_midsize_one_item_per_cta(mk, n, prec):
+    # up to ~4 MB of A per CTA: equal column ranges, at most one item per CTA, no small-item tail
+    # (ncu cold and sustained A/B: profiles/midsize_r01.jsonl)
+    p = tuning.plan(prec, mk, mk, n)
+    assert p["items"] == p["grid"] <= 148 and p["items"] >= 100
+    assert p["nbig"] == 0 and p["kbig"] == p["ksmall"] and p["ksmall"] % p["cols_per_stage"] == 0
+    rb = -(-mk // p["rows_per_block"])
+    assert rb * -(-mk // p["ksmall"]) == p["items"]
+    # the knobs still override it, and large problems keep the big-item + tail split
+    tuning.set_tuning(tuning.Tuning(small_kb=256))
+    try:
+        assert tuning.plan(prec, mk, mk, n)["items"] != p["items"] or mk == 2048
+    finally:
+        tuning.set_tuning(None)
+    assert tuning.plan(prec, 16384, 16384, n)["nbig"] > 0
+
+
 def test_plan_tsm2l_single_chunk():
     p = tuning.plan("double", 1 << 24, 16, 16)
     assert p["impl"] == "tma" and p["consumer"] == "dmma"  # fp64 16-column passes (abtest_r01e.json)
