@@ -377,6 +377,11 @@ static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
 }
 
 // Item geometry of the dynamic TMA kernel for one pass (rows_per_block = R, KC columns/stage).
+// A bytes per CTA up to which make_items uses equal items (TSM2X_MID_MB overrides, read once)
+static double mid_size_cap() {
+  static const double v = env_int("TSM2X_MID_MB", 24) * 1048576.0;
+  return v;
+}
 static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, int nt, const Tuning& tu, Items* it,
                        int64_t* grid) {
   const int64_t G_full = sms;  // one CTA per SM (smem-bound by design)
@@ -406,12 +411,13 @@ static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, 
     it->nsmall = 1;
     it->ksmall = (int64_t)align_up((size_t)k, KC);
     it->batch = std::max<int64_t>(1, (int64_t)(batch_b / ((double)k * col_bytes)));
-  } else if (tu.small_kb == 0 && tu.big_kb == 0 && tu.tail_pct == 0 && per_cta <= 4.0 * 1024 * 1024) {
-    // mid-size problems (A up to ~600 MB): about one item per CTA, equal column ranges per row
-    // block. Per-item epilogues and the ramp, not HBM, set the time here; the queue's tail
-    // balancing buys nothing (ncu, cold: 2048^2 n=16 25 -> 17 us, 4096^2 n=16 36 -> 29 us,
-    // 6144^2 n=16 69 -> 51 us, 8192^2 n=16 95 -> 83-87 us, n=8 -3 to -12 %;
-    // profiles/midsize_r01.jsonl)
+  } else if (tu.small_kb == 0 && tu.big_kb == 0 && tu.tail_pct == 0 && per_cta <= mid_size_cap()) {
+    // up to ~24 MB of A per CTA (m = k = 20480 fp64): equal column ranges per row block, in as few
+    // rounds of one item per CTA as the makespan allows. Per-item epilogues and the ramp, not
+    // HBM, bound mid-size problems, and the queue's tail balancing buys nothing there (ncu cold:
+    // 2048^2 n=16 25 -> 17 us, 4096^2 n=16 36 -> 29 us, 6144^2 n=16 69 -> 51 us; sustained: 6144^2
+    // n=16 -29 %, 8192^2 -9 / -14 %, 12288^2 -5 / -6 %, 16384^2 -2 / -3 %, 20480^2 -2 %; 30720^2
+    // unchanged within noise, so the large-problem split below stays; profiles/midsize_r01.jsonl)
     // pieces per row block: minimise the makespan (rounds of items per CTA x item columns, plus a
     // per-item cost of ~KC columns for the epilogue)
     int64_t c = (int64_t)align_up((size_t)k, KC);

@@ -21,8 +21,8 @@ def test_plan_config2_tsm2r():
 @pytest.mark.parametrize("mk,n,prec", [(2048, 16, "double"), (4096, 8, "double"), (6144, 16, "double"),
                                        (8192, 8, "double"), (4096, 16, "single")])
 def test_plan_midsize_one_item_per_cta(mk, n, prec):
-    # up to ~4 MB of A per CTA: equal column ranges, at most one item per CTA, no small-item tail
-    # (ncu cold and sustained A/B: profiles/midsize_r01.jsonl)
+    # mid-size problems: equal column ranges, no small-item tail; up to ~4 MB of A per CTA that is
+    # one round of at most one item per CTA (ncu cold and sustained A/B: profiles/midsize_r01.jsonl)
     p = tuning.plan(prec, mk, mk, n)
     assert p["items"] == p["grid"] <= 148 and p["items"] >= 100
     assert p["nbig"] == 0 and p["kbig"] == p["ksmall"] and p["ksmall"] % p["cols_per_stage"] == 0
@@ -34,7 +34,14 @@ def test_plan_midsize_one_item_per_cta(mk, n, prec):
         assert tuning.plan(prec, mk, mk, n)["items"] != p["items"] or mk == 2048
     finally:
         tuning.set_tuning(None)
-    assert tuning.plan(prec, 16384, 16384, n)["nbig"] > 0
+    assert tuning.plan(prec, 30720, 30720, n)["nbig"] > 0
+
+
+def test_plan_midsize_rounds():
+    # larger mid-size problems: a few equal rounds (16384^2: 32 row blocks x 9 pieces on 148 CTAs)
+    p = tuning.plan("double", 16384, 16384, 8)
+    assert p["nbig"] == 0 and p["items"] == 288 and p["grid"] == 148
+    assert p["nsmall"] * p["ksmall"] >= 16384 > (p["nsmall"] - 1) * p["ksmall"]
 
 
 def test_plan_tsm2l_single_chunk():
