@@ -46,6 +46,8 @@ B200_DEFAULTS = {
                 "plain loop for single-chunk ones); split-precision tf32 on the tensor cores (tc) "
                 "for fp32 16-column passes; FFMA2 for other fp32 n >= 2; else FMA "
                 "(sustained A/B under the 1000 W cap: profiles/envab_r01.json)",
+    "items": "up to 24 MB of A per CTA: equal column ranges per row block, count chosen for the "
+             "shortest makespan (about one item per CTA per round); above that the big/small split below",
     "small_kb": "min(512 (1024 for 16-column and fp64 DMMA passes), max(64, per-CTA share / 48))",
     "big_kb": "min(4096 (8192 for fp64 DMMA passes), max(small, per-CTA share / 6))",
     "tail_pct": "20 (10 for 16-column and fp64 DMMA passes)",
