@@ -122,6 +122,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, unsigned ns = 64) {
   while (!mbar_try_wait(bar, parity)) __nanosleep(ns);
 }
+// Warp release of a ring stage: the warp's lanes read the stage, __syncwarp, lane 0 arrives
+// (release; the barrier orders the other lanes' reads before it). compute-sanitizer racecheck does
+// not follow that __syncwarp edge and reports the producer's next write as a hazard
+// (tools/racecheck_probe.cu shows it on a minimal correct kernel), so the racecheck build
+// (-DTSM2X_RACECHECK, `make racecheck`) has every lane arrive and the barriers count lanes.
+#ifdef TSM2X_RACECHECK
+constexpr int kArrivalsPerWarp = 32;
+__device__ __forceinline__ void warp_release(uint64_t* bar) { mbar_arrive(bar); }
+#else
+constexpr int kArrivalsPerWarp = 1;
+__device__ __forceinline__ void warp_release(uint64_t* bar) {
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
+#endif
+
 // global -> shared bulk copy completing on an mbarrier; bytes % 16 == 0, both addresses 16B-aligned.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

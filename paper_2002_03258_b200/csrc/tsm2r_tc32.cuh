@@ -187,10 +187,10 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int j = 0; j < Cfg::LO_SLOTS; ++j) mbar_init(&lo_full[j], Cfg::CONV_WARPS);
+    for (int j = 0; j < Cfg::LO_SLOTS; ++j) mbar_init(&lo_full[j], Cfg::CONV_WARPS * kArrivalsPerWarp);
     for (int j = 0; j < 2; ++j) {
       mbar_init(&acc_full[j], 1);
-      mbar_init(&acc_empty[j], Cfg::CONV_WARPS);
+      mbar_init(&acc_empty[j], Cfg::CONV_WARPS * kArrivalsPerWarp);
     }
     mbar_fence_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -295,7 +295,13 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
         if (cur >= 0 && elect_one()) tc_commit(&acc_full[seg & 1]);
         __syncwarp();
         if (left == 0) {
-          const longlong2 md = meta[s];
+          // read by lane 0 (the lane elect_one picks in this converged warp, which also commits
+          // the stage's release) and broadcast: the read is then ordered before that release
+          // by program order rather than by the warp's convergence
+          longlong2 md = make_longlong2(0, 0);
+          if (lane == 0) md = meta[s];
+          md.x = __shfl_sync(0xffffffffu, md.x, 0);
+          md.y = __shfl_sync(0xffffffffu, md.y, 0);
           if (md.y < 0) break;
           cur = md.y;
           left = (int)(md.x >> 32);
@@ -382,7 +388,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[g & 1]);
+      warp_release(&acc_empty[g & 1]);
     };
     // An item's epilogue is deferred until the converters have prepared the next item's first
     // stage: by then the tensor core has finished the item's last MMAs, so the drain does not
@@ -480,7 +486,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&lo_full[slot]);
+      warp_release(&lo_full[slot]);
       TC32_DIAG(const unsigned long long t4c = clock64(); c_conv += t4c - t3c;)
       if constexpr (DEFER) finish_item();  // the previous item's epilogue, if one is pending
       TC32_DIAG(c_epi += clock64() - t4c;)

@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], Cfg::CW);
+      mbar_init(&empty[s], Cfg::CW * kArrivalsPerWarp);
     }
     mbar_fence_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -667,14 +667,14 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
           cons.load_ks(sa, sb, ks + 1, f1);
           if (ks + 1 == KS - 1) {
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
+            warp_release(&empty[s]);
           }
           cons.mma_ks(f0);
         } else {
           cons.load_ks(sa, sb, ks + 1, f0);
           if (ks + 1 == KS - 1) {
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
+            warp_release(&empty[s]);
           }
           cons.mma_ks(f1);
         }
@@ -746,7 +746,7 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
     KDIAG(const unsigned long long t2c = clock64(); c_fin += t2c - t1c;)
     cons.stage(sA + (size_t)s * Cfg::A_ELEMS, sB + (size_t)s * (Cfg::B_BYTES_PAD / sizeof(T)));
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    warp_release(&empty[s]);
     KDIAG(c_stage += clock64() - t2c; ++n_st;)
   }
   KDIAG(if (a.dbg && threadIdx.x == 32) {

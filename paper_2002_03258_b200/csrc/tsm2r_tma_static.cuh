@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(TmaCfg<T, NT>::THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], Cfg::CW);
+      mbar_init(&empty[s], Cfg::CW * kArrivalsPerWarp);
     }
     mbar_fence_init();
   }
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(TmaCfg<T, NT>::THREADS, 1)
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      warp_release(&empty[s]);
     }
 
     const int64_t row0 = rb * R + lrow;
