@@ -403,7 +403,11 @@ static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, 
   // single-chunk dispatch batch: 64 KB (one row block at k=16) — burst sweep (tuning_r01.json) and
   // sustained A/B (-0.5 %) agree on it with the current kernel; 256 KB was the earlier choice
   const double batch_b = tu.batch_kb > 0 ? tu.batch_kb * 1024.0 : 64.0 * 1024;
-  if ((double)k * col_bytes <= 1024.0 * 1024 || k <= ksmall) {
+  const bool mid = tu.small_kb == 0 && tu.big_kb == 0 && tu.tail_pct == 0 && per_cta <= mid_size_cap();
+  const bool single_ok = (double)k * col_bytes <= 1024.0 * 1024 || k <= ksmall;
+  // fewer row blocks than CTAs: the equal-split rule below decides whether to split (an unsplit
+  // fp32 512 x 512 x 16 ran on one CTA: 45 us vs 12 us for cuBLAS)
+  if (single_ok && !(mid && it->num_rb < G_full)) {
     // single-chunk row blocks (TSM2L shapes): no split, batched dispatch
     it->nbig = 0;
     it->kbig = KC;
@@ -411,7 +415,7 @@ static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, 
     it->nsmall = 1;
     it->ksmall = (int64_t)align_up((size_t)k, KC);
     it->batch = std::max<int64_t>(1, (int64_t)(batch_b / ((double)k * col_bytes)));
-  } else if (tu.small_kb == 0 && tu.big_kb == 0 && tu.tail_pct == 0 && per_cta <= mid_size_cap()) {
+  } else if (mid) {
     // up to ~24 MB of A per CTA (m = k = 20480 fp64): equal column ranges per row block, in as few
     // rounds of one item per CTA as the makespan allows. Per-item epilogues and the ramp, not
     // HBM, bound mid-size problems, and the queue's tail balancing buys nothing there (ncu cold:

@@ -37,6 +37,18 @@ def test_plan_midsize_one_item_per_cta(mk, n, prec):
     assert tuning.plan(prec, 30720, 30720, n)["nbig"] > 0
 
 
+def test_plan_few_row_blocks_split():
+    # fewer row blocks than CTAs: short-k shapes are split across CTAs too (fp32 512^2 x 16 used
+    # to run on one CTA), while TSM2L shapes (k within one stage) stay single-chunk
+    p = tuning.plan("single", 512, 512, 16)
+    assert p["items"] == p["grid"] == 32 and p["nsmall"] == 32
+    p = tuning.plan("double", 1000, 200, 8)
+    assert p["nsmall"] > 1 and p["grid"] == p["items"]
+    p = tuning.plan("double", 4096, 16, 16)
+    assert p["nsmall"] == 1 and p["items"] == 8
+    assert tuning.plan("double", 51200, 64, 8)["nsmall"] == 1  # 100 row blocks: splitting buys nothing
+
+
 def test_plan_midsize_rounds():
     # larger mid-size problems: a few equal rounds (16384^2: 32 row blocks x 9 pieces on 148 CTAs)
     p = tuning.plan("double", 16384, 16384, 8)
