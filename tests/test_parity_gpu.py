@@ -282,6 +282,40 @@ def test_host_path_pinned_and_pageable_slabs():
             _check(out[rows], ref, k, "double", what=(m, k, n, pinned))
 
 
+@pytest.mark.parametrize("m,k,n,prec", [(6144, 6144, 16, "double"), (16384, 16384, 8, "double"),
+                                         (12345, 9999, 13, "double"), (8192, 8192, 16, "single"),
+                                         (700, 3000, 16, "single"), (1000, 200, 8, "double")])
+def test_equal_split_regimes(m, k, n, prec):
+    """The equal-item split (make_items: up to 24 MB of A per CTA, or fewer row blocks than SMs):
+    one round, several rounds (16384^2: 288 items on 148 CTAs), ragged rows / columns, and the
+    short-k shapes that used to stay on one CTA — sampled row slabs against the oracle and the
+    whole result against cuBLAS, with C += A·B over a nonzero C."""
+    import torch
+    from oracle.rng import uniform_block
+    tsm = _tsm()
+    dt = torch.float64 if prec == "double" else torch.float32
+    npdt = np.float64 if prec == "double" else np.float32
+    A = tsm.colmajor_empty(m, k, dt, "cuda")
+    tsm.fill_uniform(A, seed=31)
+    B = tsm.colmajor_empty(k, n, dt, "cuda")
+    tsm.fill_uniform(B, seed=32)
+    C = tsm.colmajor_empty(m, n, dt, "cuda")
+    tsm.fill_uniform(C, seed=33)
+    C0 = C.clone()
+    tsm.gemm(A, B, C)
+    torch.cuda.synchronize()
+    Bh = uniform_block(range(k), range(n), 32).astype(npdt)
+    Ch = C.cpu().numpy()
+    C0h = C0.cpu().numpy()
+    for r0 in sorted({0, m // 3, max(0, m - 97)}):
+        rows = range(r0, min(m, r0 + 97))
+        Ah = uniform_block(rows, range(k), 31).astype(npdt)
+        ref = naive_gemm(Ah, Bh, C0h[r0:r0 + len(rows)])
+        _check(Ch[r0:r0 + len(rows)], ref, k, prec, what=("slab", m, k, n, r0))
+    full = (C0.double() + A.double() @ B.double()).cpu().numpy()
+    assert rel_frobenius(Ch, full) <= (1e-12 if prec == "double" else 1e-5)
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("n", [2, 4, 8, 16])
 def test_config2_sampled_rows(n):
