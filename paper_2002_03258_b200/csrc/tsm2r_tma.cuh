@@ -25,6 +25,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "tsm2r_stream.cuh"
 
@@ -124,6 +126,19 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+// Consumers that take A in the swizzled layout (DmmaConsumer<..., SWZ = true>) declare kSwz.
+template <typename C, typename = void>
+struct SwzOf : std::false_type {};
+template <typename C>
+struct SwzOf<C, std::void_t<decltype(C::kSwz)>> : std::integral_constant<bool, C::kSwz> {};
 
 __device__ __forceinline__ void red_add(double* p, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
@@ -333,10 +348,22 @@ struct Ffma2Consumer {
 // so each B fragment is one LDS.64 per lane. 32 DMMAs per warp per stage replace 256 DFMAs and
 // 64 LDS.128 of the FMA consumer; the FP64 datapath is shared (measured), so this buys issue
 // slots and power, not peak.
-template <int NT, int CW_ = 8, bool PIPE_ = false, int SB_ = 32768>
+//
+// SWZ (the default geometry): A arrives as one 3-D TMA box {16 rows, KC columns, 32 row chunks}
+// with the 128-byte swizzle, i.e. smem [chunk][column][16 rows] where the 16-byte piece p of
+// column c sits at position p ^ (c % 8). In the plain [column][row] layout every column is a
+// multiple of 128 B away from the next, so the 8 lanes of an LDS.128 phase — rows (2g, 2g+1)
+// for two g and four columns t — hit the same banks: 4-way conflicts, 16 wavefronts per
+// instruction instead of 4 (ncu at config 2: 243 M shared wavefronts, 177 M of them conflicts;
+// the smem pipe 83 % busy). With the swizzle and the k-step's four columns taken as
+// {0, 2, 4, 6} / {1, 3, 5, 7} of each 8-column group (B's fragment order permuted to match,
+// prep_dyn), a phase's eight pieces land on eight distinct positions.
+template <int NT, int CW_ = 8, bool PIPE_ = false, int SB_ = 32768, bool SWZ_ = false>
 struct DmmaConsumer {
   using Cfg = TmaCfg<double, NT, 16 / CW_, CW_, SB_>;  // R = 512 rows for CW_ in {8, 16}
   static constexpr bool kFragB = true;
+  static constexpr bool kSwz = SWZ_;
+  static_assert(!SWZ_ || Cfg::KC % 8 == 0, "swizzled layout: whole 8-column groups per stage");
   static constexpr bool kPipelined = PIPE_;  // k-step software pipeline (kernel loop below)
   static_assert(NT == 8 || NT == 16, "DMMA consumer needs NT in {8, 16}");
   static_assert(CW_ == 8 || CW_ == 16, "DMMA consumer: 8 or 16 consumer warps");
@@ -370,9 +397,19 @@ struct DmmaConsumer {
     double2 av[Q];
   };
   KDIAG(int dg = 0;)  // diagnostic build: 16 = no fragment LDS (constants), 32 = no DMMA
-  __device__ __forceinline__ void load_ks(const double* sA, const double* sB, int ks, Frag& f) const {
+  // A fragment pair (rows 2g, 2g+1 of 16-row group q, k-step column t) of k-step ks
+  __device__ __forceinline__ const double2* a_ptr(const double* sA, int ks, int q) const {
     const int g = lane >> 2, t = lane & 3;
-    const double* As = sA + (RW * warp / Cfg::BOX) * (Cfg::BOX * Cfg::KC) + (RW * warp % Cfg::BOX + 2 * g);
+    if constexpr (SWZ_) {
+      const int c = 8 * (ks >> 1) + 2 * t + (ks & 1);  // column within the stage
+      const int ch = RW * warp / 16 + q;               // 16-row chunk within the row block
+      return reinterpret_cast<const double2*>(sA + ch * (Cfg::KC * 16) + c * 16 + 2 * (g ^ (c & 7)));
+    } else {
+      const double* As = sA + (RW * warp / Cfg::BOX) * (Cfg::BOX * Cfg::KC) + (RW * warp % Cfg::BOX + 2 * g);
+      return reinterpret_cast<const double2*>(As + (4 * ks + t) * Cfg::BOX + 16 * q);
+    }
+  }
+  __device__ __forceinline__ void load_ks(const double* sA, const double* sB, int ks, Frag& f) const {
     KDIAG(if (dg & 16) {
 #pragma unroll
       for (int nt = 0; nt < NTI; ++nt) f.b[nt] = 1.0 + ks;
@@ -383,7 +420,7 @@ struct DmmaConsumer {
 #pragma unroll
     for (int nt = 0; nt < NTI; ++nt) f.b[nt] = sB[(ks * NTI + nt) * 32 + lane];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) f.av[q] = *reinterpret_cast<const double2*>(As + (4 * ks + t) * Cfg::BOX + 16 * q);
+    for (int q = 0; q < Q; ++q) f.av[q] = *a_ptr(sA, ks, q);
   }
   __device__ __forceinline__ void mma_ks(const Frag& f) {
     KDIAG(if (dg & 32) {
@@ -404,9 +441,6 @@ struct DmmaConsumer {
       }
   }
   __device__ __forceinline__ void stage(const double* sA, const double* sB) {
-    const int g = lane >> 2, t = lane & 3;
-    // the warp's rows start at RW * warp: TMA box (RW * warp) / 256, offset (RW * warp) % 256
-    const double* As = sA + (RW * warp / Cfg::BOX) * (Cfg::BOX * Cfg::KC) + (RW * warp % Cfg::BOX + 2 * g);
 #pragma unroll
     for (int ks = 0; ks < Cfg::KC / 4; ++ks) {
       double b[NTI];
@@ -414,7 +448,7 @@ struct DmmaConsumer {
       for (int nt = 0; nt < NTI; ++nt) b[nt] = sB[(ks * NTI + nt) * 32 + lane];
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
-        const double2 av = *reinterpret_cast<const double2*>(As + (4 * ks + t) * Cfg::BOX + 16 * q);
+        const double2 av = *a_ptr(sA, ks, q);
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt) {
           asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -591,7 +625,9 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
           a.it.decode(item, a.k, &rb, &col0, &col1);
           const int64_t row_base = rb * R;
           const int nbox = (int)min64(Cfg::NBOX, (a.m - row_base + Cfg::BOX - 1) / Cfg::BOX);
-          const uint32_t tx = (uint32_t)(nbox * Cfg::BOX * KC * (int)sizeof(T) + Cfg::B_BYTES);
+          // swizzled layout: one 3-D box per stage, always full (out-of-range chunks zero-filled)
+          const uint32_t tx = SwzOf<Consumer>::value ? (uint32_t)(Cfg::A_BYTES + Cfg::B_BYTES)
+                                                     : (uint32_t)(nbox * Cfg::BOX * KC * (int)sizeof(T) + Cfg::B_BYTES);
           const int64_t nst = (col1 - col0 + KC - 1) / KC;
           for (int64_t col = col0; col < col1; col += KC, ++it) {
             const int s = it % STAGES;
@@ -599,9 +635,13 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
             mbar_wait(&empty[s], ph ^ 1u);
             meta[s] = make_longlong2(rb | (nst << 32), item);
             mbar_arrive_expect_tx(&full[s], tx);
-            for (int b = 0; b < nbox; ++b)
-              tma_load_2d(sA + (size_t)s * Cfg::A_ELEMS + b * (Cfg::BOX * KC), &tmA, (int)(row_base + b * Cfg::BOX),
-                          (int)col, &full[s], pol);
+            if constexpr (SwzOf<Consumer>::value) {
+              tma_load_3d(sA + (size_t)s * Cfg::A_ELEMS, &tmA, 0, (int)col, (int)(row_base / 16), &full[s], pol);
+            } else {
+              for (int b = 0; b < nbox; ++b)
+                tma_load_2d(sA + (size_t)s * Cfg::A_ELEMS + b * (Cfg::BOX * KC), &tmA, (int)(row_base + b * Cfg::BOX),
+                            (int)col, &full[s], pol);
+            }
             if (prep_done) {
               bulk_g2s(sB + (size_t)s * (Cfg::B_BYTES_PAD / sizeof(T)), a.Bt + col * NT, Cfg::B_BYTES, &full[s]);
             } else {
@@ -780,9 +820,10 @@ __global__ void prep_bfrag(const double* __restrict__ B, int64_t ldb, int64_t k,
 // One prep launch per pass of the dynamic kernel: Bt (row-major, or DMMA fragment order when
 // FRAG) and, for split row blocks, the zeroed accumulation target (C itself for fp64 under the
 // zero-C contract, or the fp64 accumulator for fp32) — zrows x zcols at zp with leading dim zld.
+// swz: the swizzled DMMA layout's k-step order (k-step kg takes columns 8 (kg / 2) + 2t + kg % 2).
 template <typename T, int NT, bool FRAG, typename Z>
 __global__ void prep_dyn(const T* __restrict__ B, int64_t ldb, int64_t k, int64_t kpad, int w, T* __restrict__ Bt,
-                         Z* __restrict__ zp, int64_t zld, int64_t zrows, int zcols) {
+                         Z* __restrict__ zp, int64_t zld, int64_t zrows, int zcols, int swz = 0) {
   pdl_launch_dependents();
   const int64_t nb = kpad * NT, nz = zp ? zrows * zcols : 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -792,7 +833,8 @@ __global__ void prep_dyn(const T* __restrict__ B, int64_t ldb, int64_t k, int64_
         const int lane = (int)(i % 32);
         const int64_t tile = i / 32;
         const int nt = (int)(tile % (NT / 8));
-        const int64_t row = 4 * (tile / (NT / 8)) + (lane & 3);
+        const int64_t kg = tile / (NT / 8);
+        const int64_t row = swz ? 8 * (kg >> 1) + 2 * (lane & 3) + (kg & 1) : 4 * kg + (lane & 3);
         const int col = 8 * nt + (lane >> 2);
         Bt[i] = (row < k && col < w) ? B[row + col * ldb] : T(0);
       } else {

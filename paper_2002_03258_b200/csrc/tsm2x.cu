@@ -229,6 +229,35 @@ static int encode_a_map(CUtensorMap* map, const void* A, int64_t m, int64_t k, i
   return TSM2X_OK;
 }
 
+// A as a 3-D tensor {16 rows, k columns, ceil(m/16) row chunks} for the swizzled DMMA layout
+// (DmmaConsumer<..., SWZ = true>): a box {16, KC, R/16} lands as [chunk][column][16 rows] with the
+// 128-byte swizzle. Needs lda >= roundup(m, 16) (the last chunk's rows past m are read, never
+// stored) — swz_layout_ok.
+static bool swz_layout_ok(const void* A, int64_t m, int64_t lda) {
+  return aligned16(A) && (lda % 2) == 0 && lda >= (m + 15) / 16 * 16 && env_int("TSM2X_SWZ", 1) != 0;
+}
+static int encode_a_map_swz(CUtensorMap* map, const double* A, int64_t m, int64_t k, int64_t lda, int kc, int r) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!encode) return fail(TSM2X_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  cuuint64_t dims[3] = {16, (cuuint64_t)k, (cuuint64_t)((m + 15) / 16)};
+  cuuint64_t strides[2] = {(cuuint64_t)(lda * 8), 128};
+  cuuint32_t box[3] = {16, (cuuint32_t)kc, (cuuint32_t)(r / 16)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult res = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(A), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (res != CUDA_SUCCESS) return fail(TSM2X_ECUDA, "cuTensorMapEncodeTiled (swizzled fp64) failed (%d)", (int)res);
+  return TSM2X_OK;
+}
+
 // A as a 3-D tensor {32 rows, k columns, ceil(m/32) row chunks} for tsm2r_stream_tc32: a box
 // {32, 16, 16} lands in smem as [chunk][column][32 rows] with the 128B / 32B-atom swizzle — the
 // UMMA SWIZZLE_128B_BASE32B MN-major layout. Needs lda >= roundup(m, 32) (the last chunk's rows
@@ -334,7 +363,8 @@ static Tuning current_tuning() {
 // issue slots and less energy per FMA than DFMA), split-precision tf32 tensor cores for fp32
 // 16-column passes, packed FFMA2 for other fp32 widths, plain FMA otherwise.
 // TSM2X_CONSUMER=fma|dmma|ffma2|tc in the environment overrides (ablation runs).
-enum ConsumerKind { kFma = 0, kDmma = 1, kFfma2 = 2, kNull = 3, kTc = 4, kDmmaP = 5 };
+// kDmmaS / kDmmaPS: kDmma / kDmmaP on the swizzled A layout (internal; chosen by layout, not tuning)
+enum ConsumerKind { kFma = 0, kDmma = 1, kFfma2 = 2, kNull = 3, kTc = 4, kDmmaP = 5, kDmmaS = 6, kDmmaPS = 7 };
 
 static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
   static const int env = [] {
@@ -474,6 +504,18 @@ struct ConsumerFor<double, NT, kDmmaP, RPT, CW, SB> {
                                          DmmaConsumer<(NT >= 8 ? NT : 8), (CW == 16 ? 16 : 8), true, SB>,
                                          FmaConsumer<double, NT, RPT, CW, SB>>::type;
 };
+template <int NT, int RPT, int CW, int SB>
+struct ConsumerFor<double, NT, kDmmaS, RPT, CW, SB> {
+  using type = typename std::conditional<((NT == 8 || NT == 16) && RPT * CW == 16 && CW == 8 && SB == 65536),
+                                         DmmaConsumer<(NT >= 8 ? NT : 8), 8, false, 65536, true>,
+                                         FmaConsumer<double, NT, RPT, CW, SB>>::type;
+};
+template <int NT, int RPT, int CW, int SB>
+struct ConsumerFor<double, NT, kDmmaPS, RPT, CW, SB> {
+  using type = typename std::conditional<((NT == 8 || NT == 16) && RPT * CW == 16 && CW == 8 && SB == 65536),
+                                         DmmaConsumer<(NT >= 8 ? NT : 8), 8, true, 65536, true>,
+                                         FmaConsumer<double, NT, RPT, CW, SB>>::type;
+};
 template <typename T, int NT, int RPT, int CW, int SB>
 struct ConsumerFor<T, NT, kNull, RPT, CW, SB> {
   using type = NullConsumer<T, NT, RPT, CW, SB>;
@@ -540,6 +582,10 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   if ((kind == kDmma || kind == kDmmaP) && !(RPT * CW == 16 && (CW == 8 || CW == 16))) kind = kFma;
   if (kind == kFfma2 && (RPT != Vec<T>::N || CW != 8 || SB != 32768)) kind = kFma;
   if (kind == kTc) kind = (sizeof(T) == 4 && RPT == Vec<T>::N && CW == 8 && NT >= 2) ? kFfma2 : kFma;  // tc path not taken
+  // the default DMMA geometry reads A through the swizzled layout when the leading dimension
+  // allows it (bank-conflict-free fragment loads; DmmaConsumer)
+  const bool swz = sizeof(T) == 8 && (kind == kDmma || kind == kDmmaP) && RPT * CW == 16 && CW == 8 && SB == 65536 &&
+                   (NT == 8 || NT == 16) && swz_layout_ok(A, m, lda);
   const size_t bt_bytes = align_up((size_t)kpad * NT * sizeof(T), 256);
   TSM2X_TRY(ws_reserve(ws, bt_bytes + acc_bytes, (size_t)it.num_rb + 8, s));
   a.tickets = reinterpret_cast<unsigned*>(ws->counters + 8);  // zero between launches
@@ -562,7 +608,8 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, (int64_t)di.sms * 16));
     if constexpr (sizeof(T) == 8 && (NT == 8 || NT == 16)) {
       if (kind == kDmma || kind == kDmmaP) {
-        prep_dyn<T, NT, true, double><<<grid, 256, 0, s>>>(B, ldb, k, kpad, w, const_cast<T*>(a.Bt), zp, zld, zrows, w);
+        prep_dyn<T, NT, true, double>
+            <<<grid, 256, 0, s>>>(B, ldb, k, kpad, w, const_cast<T*>(a.Bt), zp, zld, zrows, w, swz ? 1 : 0);
         TSM2X_TRY(check_launch("prep_dyn"));
       } else {
         prep_dyn<T, NT, false, double><<<grid, 256, 0, s>>>(B, ldb, k, kpad, w, const_cast<T*>(a.Bt), zp, zld, zrows, w);
@@ -584,10 +631,17 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   }
 #endif
   alignas(64) CUtensorMap tmap;
-  TSM2X_TRY(encode_a_map(&tmap, A, m, k, lda, eb, Cfg::BOX, Cfg::KC));
+  if (swz)
+    TSM2X_TRY(encode_a_map_swz(&tmap, reinterpret_cast<const double*>(A), m, k, lda, Cfg::KC, Cfg::R));
+  else
+    TSM2X_TRY(encode_a_map(&tmap, A, m, k, lda, eb, Cfg::BOX, Cfg::KC));
   const bool timed = t_ev_start && t_ev_stop;
   if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
-  if (kind == kDmma)
+  if (swz && kind == kDmma)
+    TSM2X_TRY((launch_tma_kernel<T, NT, kDmmaS, RPT, CW, SB>(a, tmap, G, s)));
+  else if (swz && kind == kDmmaP)
+    TSM2X_TRY((launch_tma_kernel<T, NT, kDmmaPS, RPT, CW, SB>(a, tmap, G, s)));
+  else if (kind == kDmma)
     TSM2X_TRY((launch_tma_kernel<T, NT, kDmma, RPT, CW, SB>(a, tmap, G, s)));
   else if (kind == kDmmaP)
     TSM2X_TRY((launch_tma_kernel<T, NT, kDmmaP, RPT, CW, SB>(a, tmap, G, s)));
