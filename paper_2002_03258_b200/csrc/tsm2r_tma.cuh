@@ -344,7 +344,7 @@ struct Ffma2Consumer {
 // DMMA (fp64, NT in {8, 16}): the FP64 tensor-core MMA m8n8k4 (DMMA.8x8x4). Warp w owns rows
 // [64w, 64w+64) of the row block as four 16-row groups; one LDS.128 per lane loads rows
 // (2g, 2g+1) of column t of a group — two A fragments (M tiles of the even and the odd rows) for
-// 8 lanes x 4 columns, 4 conflict-free wavefronts. Bt is staged in fragment order (prep_bfrag)
+// 8 lanes x 4 columns (4 wavefronts when conflict-free: see SWZ below). Bt is staged in fragment order (prep_bfrag)
 // so each B fragment is one LDS.64 per lane. 32 DMMAs per warp per stage replace 256 DFMAs and
 // 64 LDS.128 of the FMA consumer; the FP64 datapath is shared (measured), so this buys issue
 // slots and power, not peak.
