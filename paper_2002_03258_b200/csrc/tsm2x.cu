@@ -406,6 +406,16 @@ static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
   return kFma;
 }
 
+// fp64 3- and 4-column passes run on the DMMA kernel's 8-column tile (B zero-padded): since the
+// swizzled layout a DMMA call at n=8 costs less energy than a DFMA one at n=4 (profiles/
+// energy_r01.log), so under the power cap: sustained 30720^2 n=4 -4.2 %, n=3 -3.9 %, TSM2L
+// 2^25 x 16 x 4 -8.1 % (profiles/swizzle_r01.txt). Not when a consumer is forced (tuning knob or
+// TSM2X_CONSUMER); TSM2X_N4_DMMA=0 turns it off.
+static bool n4_on_dmma(const Tuning& tu) {
+  static const bool on = env_int("TSM2X_N4_DMMA", 1) != 0 && getenv("TSM2X_CONSUMER") == nullptr;
+  return on && tu.consumer == 0 && tu.combine != 3;
+}
+
 // Item geometry of the dynamic TMA kernel for one pass (rows_per_block = R, KC columns/stage).
 // A bytes per CTA up to which make_items uses equal items (TSM2X_MID_MB overrides, read once)
 static double mid_size_cap() {
@@ -1052,7 +1062,10 @@ static int run_device(int variant, int64_t m, int64_t k, int64_t n, const T* A, 
   if (use_l && k > TSM2L_KMAX) return fail(TSM2X_EINVAL, "TSM2L kernel needs k <= %d, got %lld", TSM2L_KMAX, (long long)k);
   for (int64_t p = 0; p < n; p += 16) {
     const int w = (int)std::min<int64_t>(16, n - p);
-    const int nt = nt_for(w);
+    int nt = nt_for(w);
+    if (sizeof(T) == 8 && nt == 4 && !use_l && tma_layout && (impl == TSM2X_IMPL_AUTO || impl == TSM2X_IMPL_STREAM_TMA) &&
+        n4_on_dmma(current_tuning()))
+      nt = 8;
     const T* Bp = B + p * ldb;
     T* Cp = C + p * ldc;
     int rc;
@@ -1529,7 +1542,7 @@ int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, 
   memset(out, 0, sizeof(*out));
   const size_t eb = precision == TSM2X_DOUBLE ? 8 : 4;
   const int w = (int)std::min<int64_t>(16, n);
-  const int nt = nt_for(w);
+  int nt = nt_for(w);
   out->cols_per_pass = nt;
   out->passes = (int)((n + 15) / 16);
   int sms = 148;
@@ -1556,6 +1569,7 @@ int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, 
     return TSM2X_OK;
   }
   out->impl = TSM2X_IMPL_STREAM_TMA;
+  if (eb == 8 && nt == 4 && n4_on_dmma(current_tuning())) out->cols_per_pass = nt = 8;  // as run_device
   const int R = 256 * (int)(16 / eb);
   out->rows_per_block = R;
   const bool stage64 = eb == 8 && (nt == 8 || nt == 16) && getenv("TSM2X_STAGE_KB") == nullptr;

@@ -14,8 +14,17 @@ def test_plan_config2_tsm2r():
     assert p["nbig"] > 0 and p["nsmall"] > 0 and p["batch"] == 1
     # the small items cover roughly the last 10% of each row block's columns (DMMA passes)
     assert 0.08 <= p["nsmall"] * p["ksmall"] / 30720 <= 0.2
-    assert tuning.plan("double", 30720, 30720, 4)["nsmall"] * tuning.plan("double", 30720, 30720, 4)["ksmall"] \
-        >= 0.15 * 30720  # DFMA passes keep the 20 % tail
+    # fp64 3-4 column passes run on the DMMA kernel's 8-column tile (swizzle_r01.txt); n=2 stays on
+    # DFMA and keeps the 20 % tail
+    p4 = tuning.plan("double", 30720, 30720, 4)
+    assert p4["consumer"] == "dmmap" and p4["cols_per_pass"] == 8
+    assert tuning.plan("double", 30720, 30720, 2)["nsmall"] * tuning.plan("double", 30720, 30720, 2)["ksmall"] \
+        >= 0.15 * 30720
+    tuning.set_tuning(tuning.Tuning(consumer=1))
+    try:
+        assert tuning.plan("double", 30720, 30720, 4)["consumer"] == "fma"  # a forced consumer keeps the 4-column pass
+    finally:
+        tuning.set_tuning(None)
 
 
 @pytest.mark.parametrize("mk,n,prec", [(2048, 16, "double"), (4096, 8, "double"), (6144, 16, "double"),
@@ -62,7 +71,8 @@ def test_plan_tsm2l_single_chunk():
     assert p["nbig"] == 0 and p["nsmall"] == 1 and p["batch"] == 1  # 64 KB grabs = one 512x16 row block
     assert tuning.plan("double", 1 << 24, 4, 16)["batch"] == 4
     assert tuning.plan("double", 1 << 24, 16, 8)["consumer"] == "dmma"
-    assert tuning.plan("double", 1 << 24, 16, 4)["consumer"] == "fma"
+    assert tuning.plan("double", 1 << 24, 16, 4)["consumer"] == "dmma"  # 8-column DMMA tile
+    assert tuning.plan("double", 1 << 24, 16, 2)["consumer"] == "fma"
 
 
 def test_plan_fp32_and_wide():

@@ -25,6 +25,8 @@ CFGS = {
     "f16": (32768, 32768, 16, "single", False),
     "f8": (32768, 32768, 8, "single", False),
     "l16f": (1 << 24, 16, 16, "single", True),
+    "l4": (1 << 25, 16, 4, "double", True),
+    "r3": (30720, 30720, 3, "double", False),
 }
 
 
