@@ -42,7 +42,8 @@ IMPLS = {v: k for k, v in _lib.IMPL.items()}
 # The library's built-in defaults (tsm2x.cu make_items / pick_consumer_rt), stated here for
 # reporting; 0 in a Tuning means "use these".
 B200_DEFAULTS = {
-    "consumer": "auto: DMMA for fp64 8- and 16-column passes (k-step pipelined loop for split row blocks, "
+    "consumer": "auto: DMMA for fp64 8- and 16-column passes, and 3-4 column ones on the 8-column tile "
+                "(k-step pipelined loop for split row blocks, "
                 "plain loop for single-chunk ones); split-precision tf32 on the tensor cores (tc) "
                 "for fp32 16-column passes; FFMA2 for other fp32 n >= 2; else FMA "
                 "(sustained A/B under the 1000 W cap: profiles/envab_r01.json)",
