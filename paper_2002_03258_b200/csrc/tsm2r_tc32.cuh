@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_launch_dependents();  // only tsm2_finalize is launched as a programmatic dependent
   const uint32_t tmem = *tmem_slot;
   // Programmatic dependent launch as in tsm2r_stream_tma: the producer fills the ring with A
   // before waiting for the prep kernel (Bcat, zeroed accumulator); the other warps wait at once.

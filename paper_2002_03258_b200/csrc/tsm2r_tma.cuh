@@ -594,6 +594,7 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
   }
   __syncthreads();
+  pdl_launch_dependents();  // only tsm2_finalize is launched as a programmatic dependent
   // Programmatic dependent launch: Bt and the zeroed accumulation target come from the prep
   // kernel, A does not. The producer fills the ring with A tiles first and waits for prep only
   // before the first Bt copy is due (the stage barriers expect both); the consumers wait at once
@@ -853,6 +854,7 @@ __global__ void prep_dyn(const T* __restrict__ B, int64_t ldb, int64_t k, int64_
 template <typename T>
 __global__ void tsm2_finalize(const double* __restrict__ acc, int64_t ldacc, T* C, int64_t ldc, int64_t m, int w,
                               int c_is_zero) {
+  pdl_wait();  // launched with programmatic dependent launch behind the stream kernel
   const int64_t tot = m * w;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = i / m, r = i - j * m;

@@ -406,6 +406,25 @@ static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
   return kFma;
 }
 
+// fp32 split row blocks: the fp64 accumulator -> C pass, launched with programmatic dependent
+// launch so its launch latency hides behind the stream kernel's tail (the stream kernels trigger
+// their dependents once every CTA is resident; tsm2_finalize waits for their completion).
+template <typename T>
+static int launch_finalize(unsigned grid, const double* acc, int64_t ldacc, T* C, int64_t ldc, int64_t m, int w,
+                           int c_is_zero, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TSM2X_CUDA(cudaLaunchKernelEx(&cfg, tsm2_finalize<T>, acc, ldacc, C, ldc, m, w, c_is_zero));
+  return check_launch("tsm2_finalize");
+}
+
 // fp64 3- and 4-column passes run on the DMMA kernel's 8-column tile (B zero-padded): since the
 // swizzled layout a DMMA call at n=8 costs less energy than a DFMA one at n=4 (profiles/
 // energy_r01.log), so under the power cap: sustained 30720^2 n=4 -4.2 %, n=3 -3.9 %, TSM2L
@@ -678,8 +697,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   if (atomic_split && sizeof(T) == 4) {
     const int64_t tot = m * w;
     const unsigned grid = (unsigned)std::min<int64_t>((tot + 255) / 256, (int64_t)di.sms * 8);
-    tsm2_finalize<T><<<grid, 256, 0, s>>>(a.acc, a.ldacc, C, ldc, m, w, a.c_is_zero);
-    TSM2X_TRY(check_launch("tsm2_finalize"));
+    TSM2X_TRY(launch_finalize<T>(grid, a.acc, a.ldacc, C, ldc, m, w, a.c_is_zero, s));
   }
   return TSM2X_OK;
 }
@@ -778,8 +796,7 @@ static int run_tsm2r_tc32(const DevInfo& di, Workspace* ws, int64_t m, int64_t k
   if (split) {
     const int64_t tot = m * w;
     const unsigned grid = (unsigned)std::min<int64_t>((tot + 255) / 256, (int64_t)di.sms * 8);
-    tsm2_finalize<float><<<grid, 256, 0, s>>>(a.acc, a.ldacc, C, ldc, m, w, a.c_is_zero);
-    TSM2X_TRY(check_launch("tsm2_finalize"));
+    TSM2X_TRY(launch_finalize<float>(grid, a.acc, a.ldacc, C, ldc, m, w, a.c_is_zero, s));
   }
   return TSM2X_OK;
 }
