@@ -234,7 +234,8 @@ static int encode_a_map(CUtensorMap* map, const void* A, int64_t m, int64_t k, i
 // 128-byte swizzle. Needs lda >= roundup(m, 16) (the last chunk's rows past m are read, never
 // stored) — swz_layout_ok.
 static bool swz_layout_ok(const void* A, int64_t m, int64_t lda) {
-  return aligned16(A) && (lda % 2) == 0 && lda >= (m + 15) / 16 * 16 && env_int("TSM2X_SWZ", 1) != 0;
+  static const bool on = env_int("TSM2X_SWZ", 1) != 0;  // TSM2X_SWZ=0: plain layout (A/B experiments)
+  return on && aligned16(A) && (lda % 2) == 0 && lda >= (m + 15) / 16 * 16;
 }
 static int encode_a_map_swz(CUtensorMap* map, const double* A, int64_t m, int64_t k, int64_t lda, int kc, int r) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
