@@ -71,8 +71,12 @@ def kernel_name(prec, m, k, n, c_is_zero):
                 "dynamic items)")
     names = {"dmma": "DMMA m8n8k4", "dmmap": "DMMA m8n8k4, k-step software pipeline", "fma": "DFMA/FFMA",
              "ffma2": "packed FFMA2"}
-    return f"tsm2r_stream_tma ({names.get(p['consumer'], p['consumer'])} consumer; dynamic items" + \
-        ("; single-chunk row blocks)" if p["nbig"] == 0 else ")")
+    # bench's operands come from colmajor_empty (lda padded to 32): the DMMA passes read A through
+    # the swizzled 3-D TMA layout unless TSM2X_SWZ=0
+    swz = p["consumer"] in ("dmma", "dmmap") and os.environ.get("TSM2X_SWZ", "1") != "0"
+    return f"tsm2r_stream_tma ({names.get(p['consumer'], p['consumer'])} consumer" + \
+        ("; swizzled A (3-D TMA box, 128B swizzle)" if swz else "") + "; dynamic items" + \
+        ("; single-chunk row blocks)" if p["nbig"] == 0 and p["nsmall"] == 1 else ")")
 
 
 def measured_peaks():
