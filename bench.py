@@ -8,15 +8,22 @@ Workload (N=1): BASELINE configs[1] at its headline point — TSM2R fp64, refere
 A m x k = 30720 x 30720, B k x n = 30720 x 8 (BASELINE naming n=30720, k=8), C m x n,
 C += A*B. One "step" = one full TSM2R call over that problem with A resident in HBM
 (7.55 GB, 60x the 126 MB L2, so no L2 flush is needed between steps).
-N > 1: weak scaling — every rank owns a 30720-row shard of a (30720*N) x 30720 A (generated on
-its device with the shared counter-based generator), B is broadcast from rank 0 over NCCL every
-step (the path's one exchange), then each rank runs the kernel on its shard. Time = max over
-ranks of the device-event time of the K steps.
+N > 1 (torchrun): the default workload scales weakly — every rank owns a 30720-row shard of a
+(30720*N) x 30720 A. --workload tsm2r_fp64_n8_65536 is BASELINE configs[4] as specified: one
+65536 x 65536 A, rows split over the ranks by multi.row_partition (strong scaling). Either way
+each rank generates its shard on its device with the shared counter-based generator, B is
+broadcast from rank 0 over NCCL inside every step (the path's one exchange; timed separately
+as "comm"), then each rank runs the kernel on its shard; no reduction (rows are independent,
+reference SPEC.md:262). Under torchrun the process group exists at N=1 too, so the NCCL path
+runs at every N. Time = max over ranks of the device-event time of the K steps.
+Workloads whose A is under 4x the L2 (tsm2r_fp64_n8_4096) flush the L2 between steps and time
+each step with its own events.
 
 The JSON line also carries: roofline (dominant kernel, CUDA events around each launch),
 cpu_baseline (the reference CPU path restated in numpy — oracle/ — on a bounded row sample, rank 0,
 N=1), e2e (same metric through the host-buffer C ABI tsm2x_run_host with pinned host buffers,
-H2D of A and D2H of C inside the timed region), clocks (NVML samples during the timed region),
+H2D of A and D2H of C inside the timed region; at N=1 also e2e.drop_in: the reference user's call
+run_native(Variant, Matrix, ...) on pageable numpy storage), comm (the B broadcast), clocks (NVML samples during the timed region),
 gpu_launches (libtsm2x launches in the timed region).
 
 --impl reference: the reference's CPU implementation of the path (run_native's vectorised body,
@@ -42,17 +49,50 @@ METRIC = "TSM2R/TSM2L fp64 GFLOP/s and achieved HBM GB/s (% roofline) at 1/2/4/8
 UNIT = "GFLOP/s"
 
 WORKLOADS = {
-    # name: (rows per GPU m, k, n, precision, variant, c_is_zero, description)
+    # name: (rows m — per GPU for weak scaling, whole problem for strong — k, n, precision,
+    #        variant, c_is_zero, description, scaling)
     "tsm2r_fp64_n8": (30720, 30720, 8, "double", "v3", False,
-                      "TSM2R fp64, ref (m,k,n)=(30720,30720,8) = BASELINE configs[1] n=30720,k=8; C += A*B"),
-    "tsm2r_fp64_n2": (30720, 30720, 2, "double", "v3", False, "TSM2R fp64 BASELINE configs[1] k=2"),
-    "tsm2r_fp64_n4": (30720, 30720, 4, "double", "v3", False, "TSM2R fp64 BASELINE configs[1] k=4"),
-    "tsm2r_fp64_n16": (30720, 30720, 16, "double", "v3", False, "TSM2R fp64 BASELINE configs[1] k=16"),
+                      "TSM2R fp64, ref (m,k,n)=(30720,30720,8) = BASELINE configs[1] n=30720,k=8; C += A*B", "weak"),
+    "tsm2r_fp64_n2": (30720, 30720, 2, "double", "v3", False, "TSM2R fp64 BASELINE configs[1] k=2", "weak"),
+    "tsm2r_fp64_n4": (30720, 30720, 4, "double", "v3", False, "TSM2R fp64 BASELINE configs[1] k=4", "weak"),
+    "tsm2r_fp64_n16": (30720, 30720, 16, "double", "v3", False, "TSM2R fp64 BASELINE configs[1] k=16", "weak"),
     "tsm2l_fp64": (1 << 24, 16, 16, "double", "l-opt2", True,
-                   "TSM2L fp64 A 2^24x16, B 16x16, C = A*B (L_OPT2 zero-C contract), BASELINE configs[2]"),
-    "tsm2r_fp32_n16": (32768, 32768, 16, "single", "v3", False, "TSM2R fp32 BASELINE configs[3]"),
-    "tsm2r_fp64_n8_65536": (65536, 65536, 8, "double", "v3", False, "TSM2R fp64 BASELINE configs[4] per GPU"),
+                   "TSM2L fp64 A 2^24x16, B 16x16, C = A*B (L_OPT2 zero-C contract), BASELINE configs[2]", "weak"),
+    "tsm2r_fp32_n16": (32768, 32768, 16, "single", "v3", False, "TSM2R fp32 BASELINE configs[3]", "weak"),
+    "tsm2r_fp64_n8_65536": (65536, 65536, 8, "double", "v3", False,
+                            "TSM2R fp64 ref (m,k,n)=(65536,65536,8) = BASELINE configs[4], rows of A sharded over "
+                            "the GPUs (strong scaling), B broadcast over NCCL every step", "strong"),
+    "tsm2r_fp64_n8_4096": (4096, 4096, 8, "double", "v3", False,
+                           "TSM2R fp64 ref (m,k,n)=(4096,4096,8) = BASELINE configs[0] (the oracle config); L2 "
+                           "flushed between steps", "weak"),
 }
+L2_BYTES = 126 * (1 << 20)
+
+
+def spec(wl):
+    """(m, k, n, prec, variant, c_is_zero, desc, scaling) of a workload."""
+    return WORKLOADS[wl]
+
+
+def flush_l2_needed(m, k, eb):
+    """Inputs smaller than 4x the L2 get an L2 flush between timed steps (timing rules)."""
+    return m * k * eb < 4 * L2_BYTES
+
+
+def bench_config(wl, world):
+    """The `config` object — identical in both arms and on every N, so the driver can match them."""
+    from paper_2002_03258_b200.multi import RowShards
+    m, k, n, prec, variant, c_is_zero, desc, scaling = spec(wl)
+    eb = 8 if prec == "double" else 4
+    sh = RowShards(scaling, world, 0, m_total=m, rows_per_rank=m)
+    a_gb = sh.rows * k * eb / 1e9
+    return {"workload": desc, "scaling": scaling, "m_total": sh.m_total, "m_per_gpu": sh.rows, "k": k, "n": n,
+            "precision": prec, "variant": variant,
+            "naming": "reference (m,k,n), skinny n (SURVEY.md G1)",
+            "parallelism": f"row-shard x{world}" + (", B broadcast per step (NCCL)" if world > 1 else ""),
+            "l2": (f"L2 flushed between steps (A {a_gb:.3f} GB per GPU < 4 x 0.126 GB L2)" if flush_l2_needed(sh.rows, k, eb)
+                   else f"inputs larger than L2 (A {a_gb:.2f} GB per GPU vs 0.126 GB L2), no flush"),
+            "bytes_form": "eb*(mk+kn+mn) C write-only" if c_is_zero else "eb*(mk+kn+2mn) C read+write"}
 
 
 def algorithmic(m, k, n, eb, c_is_zero):
@@ -199,7 +239,7 @@ def host_threads():
 
 
 def run_reference_arm(args, wl):
-    m, k, n, prec, variant, c_is_zero, desc = WORKLOADS[wl]
+    m, k, n, prec, variant, c_is_zero, desc, scaling = spec(wl)
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -217,12 +257,14 @@ def run_reference_arm(args, wl):
     tot = sum(times)
     value = 2.0 * rows * cs * n * len(times) / tot / 1e9
     sample = (f"A[:{rows}, :{cs}] of the {m} x {k} A per step (n={n}, {prec}); reference run_native body "
-              f"(kernels.py:391-416) restated in numpy (oracle/reference.py), row slabs on {threads} threads")
+              f"(kernels.py:391-416) restated in numpy (oracle/reference.py), row slabs on {threads} threads "
+              f"(the reference itself is single-threaded numpy, so this arm is {threads}x generous to it); the "
+              f"rate is per element of A, linear in the columns sampled, so it extrapolates to the full k")
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / len(times), 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": "f64" if prec == "double" else "f32", "data": "synthetic (counter-based U[0,1))",
-            "config": {"workload": desc, "m": m, "k": k, "n": n},
+            "config": bench_config(wl, args.gpus), "sample": sample,
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": sample},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -236,33 +278,39 @@ def run_ours(args, wl):
 
     import paper_2002_03258_b200 as tsm
     from paper_2002_03258_b200 import _lib
-    from paper_2002_03258_b200.multi import broadcast_b
+    from paper_2002_03258_b200.multi import RowShards, broadcast_b, colmajor_buffer
 
-    m, k, n, prec, variant, c_is_zero, desc = WORKLOADS[wl]
+    m_cfg, k, n, prec, variant, c_is_zero, desc, scaling = spec(wl)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun")
-    # TSM2X_BENCH_SHARE_GPU=1 (test only): all ranks on cuda:0 over gloo, to exercise the
-    # multi-rank path on a one-GPU box; numbers from such a run are not bench values.
+    # under torchrun (RANK in the environment) the process group is always created, N=1 included,
+    # so the NCCL broadcast path runs at every N. TSM2X_BENCH_SHARE_GPU=1 (test only): all ranks on
+    # cuda:0 over gloo, to exercise the multi-rank path on a one-GPU box; not bench values.
+    distributed = "RANK" in os.environ
     share = os.environ.get("TSM2X_BENCH_SHARE_GPU") == "1"
     if share:
         local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        if share:
-            dist.init_process_group("gloo")
-        else:
+    backend = None
+    if distributed:
+        backend = "gloo" if share else "nccl"
+        if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # the log shows NCCL's rank count and transport
             dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     dt = torch.float64 if prec == "double" else torch.float32
     eb = 8 if prec == "double" else 4
     lib = _lib.load()
     stream = torch.cuda.current_stream(dev)
 
-    # ---- inputs resident in HBM (rank shard of a (m*world) x k matrix)
-    r0 = rank * m
+    # ---- inputs resident in HBM: this rank's row shard of the (m_total x k) A and (m_total x n) C
+    sh = RowShards(scaling, world, rank, m_total=m_cfg, rows_per_rank=m_cfg)
+    m, r0 = sh.rows, sh.r0
     A = tsm.colmajor_empty(m, k, dt, dev)
     tsm.fill_uniform(A, seed=1, row_offset=r0)
     B = tsm.colmajor_empty(k, n, dt, dev)
@@ -272,52 +320,75 @@ def run_ours(args, wl):
         C.zero_()
     else:
         tsm.fill_uniform(C, seed=3, row_offset=r0)
+    Bbuf = colmajor_buffer(k, n, dt, dev) if distributed else None
+    flush = flush_l2_needed(m, k, eb)
+    scratch = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if flush else None
     torch.cuda.synchronize()
 
-    def step(Bsrc, kev=None):
-        Bl = broadcast_b(Bsrc if rank == 0 else None, k, n, dt, dev) if world > 1 else Bsrc
+    def step(kev=None, bev=None):
+        if bev is not None:
+            bev[0].record(stream)
+        Bl = broadcast_b(B if rank == 0 else None, k, n, dt, dev, out=Bbuf) if distributed else B
+        if bev is not None:
+            bev[1].record(stream)
         if kev is not None:
             lib.tsm2x_set_kernel_events(ctypes.c_void_p(kev[0].cuda_event), ctypes.c_void_p(kev[1].cuda_event))
         tsm.gemm(A, Bl, C, variant=variant, c_is_zero=c_is_zero)
 
     for _ in range(args.warmup):
-        step(B)
-    kevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for a_, b_ in kevs:  # materialise the CUDA events before handing them to the library
-        a_.record(stream)
-        b_.record(stream)
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
+        step()
+    mk = lambda: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))  # noqa: E731
+    kevs = [mk() for _ in range(args.steps)]
+    bevs = [mk() for _ in range(args.steps)]
+    sevs = [mk() for _ in range(args.steps)]
+    for pair in kevs + bevs + sevs:  # materialise the CUDA events before handing them to the library
+        for e in pair:
+            e.record(stream)
+    t0, t1 = mk()
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = _lib.launch_count()
     with ClockSampler(local) as clk:
         t0.record(stream)
         for i in range(args.steps):
-            step(B, kevs[i])
+            if flush:
+                scratch.fill_(float(i))  # 252 MB written: evicts A from the 126 MB L2 (outside the step events)
+            sevs[i][0].record(stream)
+            step(kevs[i], bevs[i])
+            sevs[i][1].record(stream)
         t1.record(stream)
         torch.cuda.synchronize()
     launches = _lib.launch_count() - launches0
-    if world > 1:
+    if distributed:
         dist.barrier()
-    ms_total = t0.elapsed_time(t1)
+    # flushed runs: the sum of the per-step events (flush excluded); else the whole timed region
+    ms_total = sum(a_.elapsed_time(b_) for a_, b_ in sevs) if flush else t0.elapsed_time(t1)
     kern_ms = sum(a_.elapsed_time(b_) for a_, b_ in kevs) / args.steps
-    if world > 1:
-        t = torch.tensor([ms_total, kern_ms], device=dev, dtype=torch.float64)
+    bcast_ms = sum(a_.elapsed_time(b_) for a_, b_ in bevs) / args.steps if distributed else 0.0
+    if distributed:
+        t = torch.tensor([ms_total, kern_ms, bcast_ms], device=dev, dtype=torch.float64)
+        if backend == "gloo":
+            t = t.cpu()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total, kern_ms = float(t[0]), float(t[1])
-    flops, byts = algorithmic(m, k, n, eb, c_is_zero)
+        ms_total, kern_ms, bcast_ms = float(t[0]), float(t[1]), float(t[2])
+    flops_all, byts_all = algorithmic(sh.m_total, k, n, eb, c_is_zero)
+    byts_all += (world - 1) * k * n * eb if world > 1 else 0  # every shard reads B once
+    _, byts = algorithmic(m, k, n, eb, c_is_zero)  # this rank's kernel
     ms_step = ms_total / args.steps
-    value = flops * world / (ms_step * 1e-3) / 1e9
-    gbps = byts * world / (ms_step * 1e-3) / 1e9
+    value = flops_all / (ms_step * 1e-3) / 1e9
+    gbps = byts_all / (ms_step * 1e-3) / 1e9
     peak, peak_src = measured_peaks()
     kern_gbps = byts / (kern_ms * 1e-3) / 1e9
     traffic = ncu_traffic(wl)
 
-    # ---- e2e through the host-buffer C ABI (pinned host buffers)
+    # ---- e2e through the host-buffer C ABI (pinned host buffers), every rank its shard
     e2e = None
     if args.e2e_steps > 0:
-        e2e = run_e2e(args, A, B, C, m, k, n, dt, eb, variant, c_is_zero, world, rank, dev)
+        e2e = run_e2e(args, A, B, C, m, k, n, dt, eb, variant, c_is_zero, world, distributed, backend, dev,
+                      flops_all)
+        if world == 1 and not args.no_drop_in:
+            e2e["drop_in"] = run_drop_in(args, A, B, C, m, k, n, prec, variant, c_is_zero, flops_all)
 
     # ---- CPU baseline (rank 0, N=1)
     cpu = None
@@ -331,9 +402,9 @@ def run_ours(args, wl):
         # reference's path, context for the GPU/CPU ratio only
         tb = []
         for _ in range(3):
-            t0 = time.perf_counter()
+            t0_ = time.perf_counter()
             _ = Chh + Ah @ Bh
-            tb.append(time.perf_counter() - t0)
+            tb.append(time.perf_counter() - t0_)
         blas = 2.0 * rows * cols * n / min(tb) / 1e9
         del Ah, Bh, Chh
         cpu = {"value": round(rate, 4), "unit": UNIT, "cores": threads, "kind": "port",
@@ -345,14 +416,10 @@ def run_ours(args, wl):
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64" if prec == "double" else "f32",
             "data": "synthetic: counter-based U[0,1) generated on device (oracle/rng.py regenerates any slab)",
-            "config": {"workload": desc, "m_per_gpu": m, "m_total": m * world, "k": k, "n": n,
-                       "naming": "reference (m,k,n), skinny n (SURVEY.md G1)",
-                       "parallelism": f"row-shard x{world}" + (", B broadcast per step (NCCL)" if world > 1 else ""),
-                       "l2": f"inputs larger than L2 (A {m * k * eb / 1e9:.2f} GB per GPU vs 0.126 GB L2), no flush",
-                       "bytes_form": "eb*(mk+kn+mn) C write-only" if c_is_zero else "eb*(mk+kn+2mn) C read+write"},
+            "config": bench_config(wl, world),
             "GBps": round(gbps, 1),
             "roofline": {"bound": "hbm", "achieved": round(kern_gbps, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(kern_gbps / peak, 4), "traffic": traffic,
@@ -361,17 +428,21 @@ def run_ours(args, wl):
                          "peak_source": peak_src,
                          "read_stream_ceiling_gbs": 7300.0,
                          "frac_of_read_stream": round(kern_gbps / 7300.0, 4)},
+            "comm": ({"backend": backend, "op": "broadcast of B from rank 0 every step", "bytes": k * n * eb,
+                      "ms_per_step": round(bcast_ms, 5), "world": world} if distributed else None),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk.summary(),
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 
-def run_e2e(args, A, B, C, m, k, n, dt, eb, variant, c_is_zero, world, rank, dev):
+def run_e2e(args, A, B, C, m, k, n, dt, eb, variant, c_is_zero, world, distributed, backend, dev, flops_all):
+    """Same metric through tsm2x_run_host (the C-ABI drop-in for run_native) from pinned host
+    buffers: every step copies this rank's A shard (and B, C) host->device and C back."""
     import torch
     import torch.distributed as dist
 
@@ -400,23 +471,56 @@ def run_e2e(args, A, B, C, m, k, n, dt, eb, variant, c_is_zero, world, rank, dev
         _lib.check(rc)
 
     call()  # warm-up (allocations, staging)
-    if world > 1:
+    if distributed:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
         call()
     t = (time.perf_counter() - t0) / args.e2e_steps
-    if world > 1:
-        tt = torch.tensor([t], device=dev, dtype=torch.float64)
+    if distributed:
+        tt = torch.tensor([t], dtype=torch.float64, device="cpu" if backend == "gloo" else dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt[0])
-    flops, _ = algorithmic(m, k, n, eb, c_is_zero)
     h2d = eb * (k * m + k * n + (0 if c_is_zero else m * n))
     d2h = eb * m * n
-    return {"value": round(flops * world / t / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": round(t * 1e3, 3), "steps": args.e2e_steps,
+    del hA
+    return {"value": round(flops_all / t / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+            "d2h_bytes_per_step": d2h * world, "ms_per_step": round(t * 1e3, 3), "steps": args.e2e_steps,
             "host_buffers": "pinned" if pinned else "pageable",
-            "api": "tsm2x_run_host (C ABI drop-in for run_native), H2D of A pipelined with the kernels"}
+            "api": "tsm2x_run_host (C ABI drop-in for run_native), H2D of A pipelined with the kernels; max over ranks"}
+
+
+def run_drop_in(args, A, B, C, m, k, n, prec, variant, c_is_zero, flops_all):
+    """The reference user's call: paper_2002_03258_b200.run_native(variant, Matrix, Matrix, Matrix,
+    KernelParams) on pageable numpy storage (reference kernels.py:391-416). Matrix construction
+    (a copy of A, as the reference's Matrix.__init__ makes, core.py:93-106) is timed separately."""
+    import numpy as np
+
+    import paper_2002_03258_b200 as tsm
+    a_np = A.t().contiguous().cpu().numpy().reshape(-1)  # column-major flat, ld = m
+    b_np = B.t().contiguous().cpu().numpy().reshape(-1)
+    c_np = np.zeros(m * n, a_np.dtype) if c_is_zero else C.t().contiguous().cpu().numpy().reshape(-1)
+    t0 = time.perf_counter()
+    Am = tsm.Matrix(m, k, a_np, prec)
+    t_construct = time.perf_counter() - t0
+    del a_np
+    Bm, Cm = tsm.Matrix(k, n, b_np, prec), tsm.Matrix(m, n, c_np, prec)
+    params = tsm.KernelParams(t1=128, t2=n, t3=4, tcf=1, variant=tsm.Variant.parse(variant))
+    v = tsm.Variant.parse(variant)
+    tsm.run_native(v, Am, Bm, Cm, params)  # warm-up (pinned staging buffers, device buffers)
+    steps = max(1, args.e2e_steps)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        out = tsm.run_native(v, Am, Bm, Cm, params)
+    t = (time.perf_counter() - t0) / steps
+    del out, Am
+    eb = 8 if prec == "double" else 4
+    return {"value": round(flops_all / t / 1e9, 3), "unit": UNIT, "ms_per_step": round(t * 1e3, 3), "steps": steps,
+            "h2d_bytes_per_step": eb * (k * m + k * n + (0 if c_is_zero else m * n)),
+            "d2h_bytes_per_step": eb * m * n, "host_buffers": "pageable (numpy Matrix storage)",
+            "matrix_construction_ms": round(t_construct * 1e3, 3),
+            "value_with_construction": round(flops_all / (t + t_construct) / 1e9, 3),
+            "api": "paper_2002_03258_b200.run_native(Variant, Matrix, Matrix, Matrix, KernelParams) -> Matrix"}
 
 
 def main():
@@ -429,6 +533,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-elems", type=int, default=1 << 26, help="elements of A in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-drop-in", action="store_true", help="skip the run_native (pageable Matrix) e2e leg")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

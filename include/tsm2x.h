@@ -81,7 +81,12 @@ enum tsm2x_impl {
 int tsm2x_validate(int variant, int64_t m, int64_t k, int64_t n, const tsm2x_params* params);
 
 /* Device-resident run. A, B, C are device pointers; stream is a cudaStream_t (NULL = legacy
- * default stream). Returns after enqueueing (asynchronous) unless CHECK_ZERO_C is set. */
+ * default stream). Returns after enqueueing (asynchronous) unless CHECK_ZERO_C is set.
+ * CUDA graphs: calls may be captured once an eager call of the same (or a larger) shape has run
+ * on the stream (its workspace is then large enough; growth during a capture is refused with
+ * TSM2X_EUNSUPPORTED). Captured calls reuse the capturing stream's workspace, so graphs
+ * captured on one stream must not replay concurrently with each other or with eager calls on
+ * that stream. */
 int tsm2x_run(int variant, int precision, int64_t m, int64_t k, int64_t n,
               const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
               const tsm2x_params* params, uint32_t flags, void* stream);

@@ -190,15 +190,36 @@ class Matrix:
         return self.storage.reshape((self.rows, self.cols), order="F")
 
     def __eq__(self, other) -> bool:
-        if not isinstance(other, Matrix):
+        """Equal to any Matrix-like object (this class or the reference's) with the same shape,
+        precision and storage bits."""
+        try:
+            rows, cols, storage = other.rows, other.cols, other.storage
+            prec = Precision.coerce(other.precision)
+        except (AttributeError, ValueError):
             return False
-        return (self.rows, self.cols, self.precision) == (other.rows, other.cols, other.precision) and bool(
-            np.array_equal(self.storage, other.storage))
+        return (self.rows, self.cols, self.precision) == (rows, cols, prec) and bool(
+            np.array_equal(self.storage, storage))
 
     __hash__ = None
 
     def __repr__(self) -> str:
         return f"Matrix({self.rows}x{self.cols}, {self.precision.value})"
+
+
+def result_like(C, rows: int, cols: int, flat: np.ndarray, precision: Precision):
+    """The result Matrix of run_native, of the caller's Matrix type: when C is a reference
+    ``tsgemm.Matrix`` (same ``__slots__`` layout, reference core.py:84-106) the result is one too,
+    so ``==`` against reference results (whose ``__eq__`` checks ``isinstance``) keeps working.
+    The freshly produced array is adopted without a copy either way."""
+    cls = type(C)
+    if cls is Matrix or not all(hasattr(C, a) for a in Matrix.__slots__):
+        return Matrix._adopt(rows, cols, flat, precision)
+    obj = cls.__new__(cls)
+    flat = flat.reshape(-1)
+    flat.flags.writeable = False
+    obj.rows, obj.cols, obj.storage = rows, cols, flat
+    obj.precision = C.precision  # the caller's Precision enum member
+    return obj
 
 
 @dataclass(frozen=True)

@@ -151,8 +151,23 @@ static Workspace* workspace_for(int dev, cudaStream_t s) {
   return slot.get();
 }
 
+// Growing the workspace inside a stream capture would bake graph-owned memory (and an un-run
+// zeroing memset) into the workspace: refuse, the caller makes one eager call of the same (or a
+// larger) shape on the stream before capturing. Graphs captured on one stream share that
+// stream's workspace (queue counters, Bt, accumulators): they must not replay concurrently with
+// each other or with eager calls on the same stream (see tsm2x.h).
 static int ws_reserve(Workspace* w, size_t bytes, size_t counters, cudaStream_t s) {
   bytes = std::max<size_t>(bytes, 1 << 20);
+  const size_t cwant = std::max<size_t>(counters + 1, 4096);
+  if (bytes > w->cap || cwant > w->ccap) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    TSM2X_CUDA(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(TSM2X_EUNSUPPORTED,
+                  "workspace of this stream must grow (%zu -> %zu bytes) during a CUDA graph capture: make one "
+                  "eager call of this shape on the stream before capturing",
+                  w->cap, std::max(bytes, w->cap));
+  }
   if (bytes > w->cap) {
     if (w->buf) TSM2X_CUDA(cudaFreeAsync(w->buf, s));
     w->buf = nullptr;
@@ -233,9 +248,35 @@ static int encode_a_map(CUtensorMap* map, const void* A, int64_t m, int64_t k, i
 // (DmmaConsumer<..., SWZ = true>): a box {16, KC, R/16} lands as [chunk][column][16 rows] with the
 // 128-byte swizzle. Needs lda >= roundup(m, 16) (the last chunk's rows past m are read, never
 // stored) — swz_layout_ok.
-static bool swz_layout_ok(const void* A, int64_t m, int64_t lda) {
+// The 3-D maps read whole row chunks: the last column's rows m .. roundup(m, chunk) - 1 are read
+// (never used). Those elements lie inside A's allocation unless A is a sub-view ending near the
+// end of its buffer (e.g. big[40:64, :] of a 64-row buffer); tail_in_allocation checks the
+// allocation range with the driver whenever m is not a chunk multiple.
+static bool tail_in_allocation(const void* A, int64_t m, int64_t k, int64_t lda, size_t eb, int64_t chunk) {
+  if (m % chunk == 0) return true;
+  using AddrRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static AddrRangeFn range = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      range = reinterpret_cast<AddrRangeFn>(fn);
+  });
+  if (!range) return false;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)A) != CUDA_SUCCESS) {
+    cudaGetLastError();
+    return false;
+  }
+  const uint64_t end = (uint64_t)(uintptr_t)A + (uint64_t)((k - 1) * lda + (m + chunk - 1) / chunk * chunk) * eb;
+  return end <= (uint64_t)base + size;
+}
+static bool swz_layout_ok(const void* A, int64_t m, int64_t k, int64_t lda) {
   static const bool on = env_int("TSM2X_SWZ", 1) != 0;  // TSM2X_SWZ=0: plain layout (A/B experiments)
-  return on && aligned16(A) && (lda % 2) == 0 && lda >= (m + 15) / 16 * 16;
+  return on && aligned16(A) && (lda % 2) == 0 && lda >= (m + 15) / 16 * 16 && tail_in_allocation(A, m, k, lda, 8, 16);
 }
 static int encode_a_map_swz(CUtensorMap* map, const double* A, int64_t m, int64_t k, int64_t lda, int kc, int r) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -615,7 +656,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   // the default DMMA geometry reads A through the swizzled layout when the leading dimension
   // allows it (bank-conflict-free fragment loads; DmmaConsumer)
   const bool swz = sizeof(T) == 8 && (kind == kDmma || kind == kDmmaP) && RPT * CW == 16 && CW == 8 && SB == 65536 &&
-                   (NT == 8 || NT == 16) && swz_layout_ok(A, m, lda);
+                   (NT == 8 || NT == 16) && swz_layout_ok(A, m, k, lda);
   const size_t bt_bytes = align_up((size_t)kpad * NT * sizeof(T), 256);
   TSM2X_TRY(ws_reserve(ws, bt_bytes + acc_bytes, (size_t)it.num_rb + 8, s));
   a.tickets = reinterpret_cast<unsigned*>(ws->counters + 8);  // zero between launches
@@ -708,7 +749,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
 // accumulator (+ tsm2_finalize), single-chunk row blocks store C directly.
 static bool tc32_ok(const float* A, int64_t m, int64_t k, int64_t lda) {
   return aligned16(A) && lda % 4 == 0 && lda >= (int64_t)align_up((size_t)m, 32) && m < (int64_t(1) << 31) &&
-         k < (int64_t(1) << 31);
+         k < (int64_t(1) << 31) && tail_in_allocation(A, m, k, lda, 4, 32);
 }
 
 static int run_tsm2r_tc32(const DevInfo& di, Workspace* ws, int64_t m, int64_t k, int w, const float* A, int64_t lda,
@@ -1337,7 +1378,7 @@ static int run_host_t(int variant, int64_t m, int64_t k, int64_t n, const T* A, 
       TSM2X_TRY(stg.copy(dA[b], ldd * eb, A + c0 * lda, lda * eb, m * eb, cw, hc->h2d));
       TSM2X_CUDA(cudaEventRecord(loaded[b], hc->h2d));
       TSM2X_CUDA(cudaStreamWaitEvent(hc->comp, loaded[b], 0));
-      const uint32_t f = (c_is_zero && j == 0) ? TSM2X_FLAG_C_IS_ZERO : 0;
+      const uint32_t f = ((c_is_zero && j == 0) ? TSM2X_FLAG_C_IS_ZERO : 0) | (flags & TSM2X_FLAG_DETERMINISTIC);
       TSM2X_TRY(run_device<T>(dev_variant, m, cw, n, dA[b], ldd, dB + c0, k, dC, ldd, params, f, TSM2X_IMPL_AUTO,
                               hc->comp));
       TSM2X_CUDA(cudaEventRecord(consumed[b], hc->comp));
@@ -1393,7 +1434,8 @@ static int run_host_t(int variant, int64_t m, int64_t k, int64_t n, const T* A, 
     TSM2X_CUDA(cudaEventRecord(loaded[b], hc->h2d));
     TSM2X_CUDA(cudaStreamWaitEvent(hc->comp, loaded[b], 0));
     TSM2X_TRY(run_device<T>(dev_variant, rw, k, n, dA[b], rs, dB, k, dC[b], rs, params,
-                            c_is_zero ? TSM2X_FLAG_C_IS_ZERO : 0, TSM2X_IMPL_AUTO, hc->comp));
+                            (c_is_zero ? TSM2X_FLAG_C_IS_ZERO : 0) | (flags & TSM2X_FLAG_DETERMINISTIC),
+                            TSM2X_IMPL_AUTO, hc->comp));
     TSM2X_CUDA(cudaEventRecord(computed[b], hc->comp));
     TSM2X_CUDA(cudaStreamWaitEvent(hc->d2h, computed[b], 0));
     if (pinnedOut) {

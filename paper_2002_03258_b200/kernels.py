@@ -22,7 +22,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .core import Matrix, Precision, Variant, check_dims, validate_params_for
+from .core import Matrix, Precision, Variant, check_dims, result_like, validate_params_for
 
 
 def _params_struct(params) -> _lib.Params:
@@ -37,20 +37,32 @@ def _flat(M, dtype) -> np.ndarray:
     return a
 
 
-def run_native(variant, A, B, C, params) -> Matrix:
-    """``C + A @ B`` on the B200 for column-major Matrix inputs (reference kernels.py:391-416)."""
+def _host_call(variant, A, B, C, params, deterministic):
+    """Validation + host arrays shared by run_native / run_native_multi."""
     variant = Variant.coerce(variant)
     m, k, n = check_dims(A, B, C)
     validate_params_for(params, m, k, n)
     prec = Precision.coerce(A.precision)
     dtype = prec.dtype
     a, b, c = _flat(A, dtype), _flat(B, dtype), _flat(C, dtype)
-    flags = 0
+    flags = _lib.FLAG_DETERMINISTIC if deterministic else 0
     if variant is Variant.L_OPT2:
         if np.any(c != 0):
             raise ValueError("L_OPT2 stores partial sums to C and requires a zeroed C")
         flags |= _lib.FLAG_C_IS_ZERO
-    out = np.empty(m * n, dtype=dtype)
+    return variant, m, k, n, prec, a, b, c, flags
+
+
+def run_native(variant, A, B, C, params, *, deterministic: bool = True) -> Matrix:
+    """``C + A @ B`` on the B200 for column-major Matrix inputs (reference kernels.py:391-416).
+
+    ``deterministic`` (default on): split row blocks combine in column order, so repeated calls
+    return the same bits, as the reference's do. The host path is bound by the PCIe copy of A,
+    so the ordered combine costs nothing measurable here (it is 5-30 % of the kernel alone).
+    The result has the caller's Matrix type (reference Matrix in, reference Matrix out).
+    """
+    variant, m, k, n, prec, a, b, c, flags = _host_call(variant, A, B, C, params, deterministic)
+    out = np.empty(m * n, dtype=prec.dtype)
     lib = _lib.load()
     p = _params_struct(params)
     rc = lib.tsm2x_run_host(
@@ -58,35 +70,25 @@ def run_native(variant, A, B, C, params) -> Matrix:
         a.ctypes.data, m, b.ctypes.data, k, c.ctypes.data, out.ctypes.data, m, ctypes.byref(p), flags,
         _current_device())
     _lib.check(rc)
-    return Matrix._adopt(m, n, out, prec)
+    return result_like(C, m, n, out, prec)
 
 
-def run_native_multi(variant, A, B, C, params, devices) -> Matrix:
+def run_native_multi(variant, A, B, C, params, devices, *, deterministic: bool = True) -> Matrix:
     """run_native over several GPUs of this process (``tsm2x_run_host_multi``): contiguous
     32-row-aligned row shards, one per entry of ``devices`` (may repeat), each streamed by its
     own host thread, so the per-GPU PCIe links add up. Same result contract as run_native."""
-    variant = Variant.coerce(variant)
-    m, k, n = check_dims(A, B, C)
-    validate_params_for(params, m, k, n)
-    prec = Precision.coerce(A.precision)
-    dtype = prec.dtype
-    a, b, c = _flat(A, dtype), _flat(B, dtype), _flat(C, dtype)
-    flags = 0
-    if variant is Variant.L_OPT2:
-        if np.any(c != 0):
-            raise ValueError("L_OPT2 stores partial sums to C and requires a zeroed C")
-        flags |= _lib.FLAG_C_IS_ZERO
+    variant, m, k, n, prec, a, b, c, flags = _host_call(variant, A, B, C, params, deterministic)
     devices = list(devices)
     if not devices:
         raise ValueError("devices must not be empty")
     devs = (ctypes.c_int * len(devices))(*devices)
-    out = np.empty(m * n, dtype=dtype)
+    out = np.empty(m * n, dtype=prec.dtype)
     p = _params_struct(params)
     rc = _lib.load().tsm2x_run_host_multi(
         variant.ordinal, _lib.DOUBLE if prec is Precision.DOUBLE else _lib.SINGLE, m, k, n, a.ctypes.data, m,
         b.ctypes.data, k, c.ctypes.data, out.ctypes.data, m, ctypes.byref(p), flags, len(devices), devs)
     _lib.check(rc)
-    return Matrix._adopt(m, n, out, prec)
+    return result_like(C, m, n, out, prec)
 
 
 def simulate(*args, **kwargs):
@@ -118,13 +120,20 @@ def colmajor_empty(rows: int, cols: int, dtype, device, pad_to: int = 32):
 
 
 def _ld(t, rows: int) -> int:
+    """Leading dimension of a column-major tensor. Layouts whose columns overlap (stride(1) <
+    rows, e.g. expand() or a stride-0 broadcast) are rejected: the kernels would read past the
+    storage or write aliased elements."""
     if t.dim() != 2:
         raise ValueError("expected a 2-D tensor")
     s0, s1 = t.stride()
     if s0 != 1 and not (t.shape[0] == 1):
         raise ValueError("tensor must be column-major (stride(0) == 1); use colmajor_empty or x.t().contiguous().t()")
-    ld = s1 if t.shape[1] > 1 else max(s1, rows)
-    return max(int(ld), rows)
+    if t.shape[1] == 1:
+        return max(int(s1), rows)  # one column: its stride is never used
+    if s1 < rows:
+        raise ValueError(f"column stride {s1} < rows {rows}: overlapping columns (expanded or broadcast tensor); "
+                         "pass a dense column-major tensor")
+    return int(s1)
 
 
 def gemm(A, B, C, *, variant=Variant.V3, params=None, c_is_zero: bool = False, impl: str = "auto",

@@ -36,13 +36,14 @@ def colmajor_buffer(rows: int, cols: int, dtype, device):
     return torch.empty((cols, rows), dtype=dtype, device=device).t()
 
 
-def broadcast_b(B, k: int, n: int, dtype, device, src: int = 0, group=None):
-    """Returns the k x n column-major B on every rank (rank ``src`` passes its B, others None)."""
-    import torch
+def broadcast_b(B, k: int, n: int, dtype, device, src: int = 0, group=None, out=None):
+    """Returns the k x n column-major B on every rank (rank ``src`` passes its B, others None).
+    ``out`` (a dense column-major k x n buffer, e.g. from :func:`colmajor_buffer`) is reused
+    instead of allocating one per call."""
     import torch.distributed as dist
     rank = dist.get_rank(group) if group is not None else dist.get_rank()
-    buf = colmajor_buffer(k, n, dtype, device)
-    if rank == src:
+    buf = colmajor_buffer(k, n, dtype, device) if out is None else out
+    if rank == src and B is not None and B.data_ptr() != buf.data_ptr():
         buf.copy_(B)
     if _host_staged(buf, group):
         host = buf.t().cpu()
@@ -60,18 +61,50 @@ def _host_staged(t, group) -> bool:
 
 
 def run_sharded(A_local, B, C_local, *, k: int, n: int, variant="v3", c_is_zero: bool = False, src: int = 0,
-                group=None, compute: Optional[Callable] = None):
+                group=None, compute: Optional[Callable] = None, b_out=None):
     """One distributed call: broadcast B from ``src``, then C_local (+)= A_local @ B on each rank.
 
     ``A_local``/``C_local`` are this rank's row shards (column-major). Returns (C_local, B_local).
     """
-    Bl = broadcast_b(B, k, n, A_local.dtype, A_local.device, src=src, group=group)
+    Bl = broadcast_b(B, k, n, A_local.dtype, A_local.device, src=src, group=group, out=b_out)
     if compute is None:
         from .kernels import gemm
         gemm(A_local, Bl, C_local, variant=variant, c_is_zero=c_is_zero)
     else:
         compute(A_local, Bl, C_local, c_is_zero)
     return C_local, Bl
+
+
+class RowShards:
+    """The row shard a rank owns in one of the two scaling modes of the multi-GPU driver.
+
+    * ``strong``: a fixed ``m_total`` x k problem (BASELINE configs[4]: 65536^2, n=8) split by
+      :func:`row_partition` — 32-row-aligned, balanced, the last shard ragged.
+    * ``weak``: every rank owns ``rows_per_rank`` rows, rank r starting at r * rows_per_rank
+      (per-GPU work fixed as the world grows).
+
+    Rows of C are independent (reference SPEC.md:262), so a shard's result is bit-identical to
+    the same rows of the whole-matrix result; the only exchange is B's broadcast.
+    """
+
+    def __init__(self, scaling: str, world: int, rank: int, *, m_total: int = 0, rows_per_rank: int = 0):
+        if scaling == "strong":
+            if m_total < 1:
+                raise ValueError("strong scaling needs m_total >= 1")
+            self.r0, self.r1 = row_partition(m_total, world, rank)
+            self.m_total = m_total
+        elif scaling == "weak":
+            if rows_per_rank < 1:
+                raise ValueError("weak scaling needs rows_per_rank >= 1")
+            self.r0, self.r1 = rank * rows_per_rank, (rank + 1) * rows_per_rank
+            self.m_total = rows_per_rank * world
+        else:
+            raise ValueError(f"unknown scaling {scaling!r}")
+        self.scaling, self.world, self.rank = scaling, world, rank
+
+    @property
+    def rows(self) -> int:
+        return self.r1 - self.r0
 
 
 def gather_c(C_local, m: int, n: int, dst: int = 0, group=None):

@@ -11,6 +11,36 @@ if ROOT not in sys.path:
 
 GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
 REFERENCE_SRC = "/root/reference/pkg/src"
+# the unmodified reference installed by tools/install_reference.sh (git-ignored; travels to the GPU
+# box with the snapshot, unlike /root/reference): the package and a copy of its own test modules
+REFERENCE_INSTALL = os.path.join(ROOT, "baseline", "_ref")
+REFERENCE_TESTS = [os.path.join(REFERENCE_INSTALL, "tsgemm_tests"), "/root/reference/pkg/tests"]
+
+
+def reference_path():
+    """Directory holding the importable reference ``tsgemm`` package, or None."""
+    for d in (REFERENCE_INSTALL, REFERENCE_SRC):
+        if os.path.isfile(os.path.join(d, "tsgemm", "__init__.py")):
+            return d
+    return None
+
+
+def reference_tests_dir():
+    for d in REFERENCE_TESTS:
+        if os.path.isfile(os.path.join(d, "test_kernels.py")):
+            return d
+    return None
+
+
+def import_reference():
+    """The reference ``tsgemm`` package (importing it with its own directory on sys.path)."""
+    d = reference_path()
+    if d is None:
+        pytest.skip("reference package not installed (tools/install_reference.sh)")
+    if d not in sys.path:
+        sys.path.append(d)
+    import tsgemm
+    return tsgemm
 
 
 def pytest_configure(config):

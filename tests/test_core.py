@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 import paper_2002_03258_b200 as tsm
-from conftest import REFERENCE_SRC
+from conftest import REFERENCE_SRC, import_reference
 from paper_2002_03258_b200.core import check_dims, validate_params_for
 
 
@@ -144,3 +144,44 @@ def test_validation_agrees_with_reference():
     rC = rcore.Matrix.zeros(8, 2, rcore.Precision.DOUBLE)
     assert check_dims(rA, rB, rC) == (8, 4, 2)
     validate_params_for(rcore.KernelParams(t1=32, t2=2, t3=4), 8, 4, 2)
+
+
+def test_matrix_equality_with_reference_matrices():
+    """Our Matrix compares equal to a reference Matrix with the same bits (duck-typed __eq__), and
+    result_like hands back the caller's Matrix type without a copy."""
+    from paper_2002_03258_b200.core import result_like
+    ts = import_reference()
+    data = np.arange(6, dtype=np.float64)
+    ours = tsm.Matrix(2, 3, data, tsm.Precision.DOUBLE)
+    ref = ts.Matrix(2, 3, data, ts.Precision.DOUBLE)
+    assert ours == ref
+    assert ours != ts.Matrix(2, 3, data + 1, ts.Precision.DOUBLE)
+    assert ours != ts.Matrix(3, 2, data, ts.Precision.DOUBLE)
+    assert ours != object()
+    flat = np.arange(6, dtype=np.float64)
+    r = result_like(ref, 2, 3, flat, tsm.Precision.DOUBLE)
+    assert type(r) is ts.Matrix and r.precision is ts.Precision.DOUBLE
+    assert r == ref and ref == r  # the reference's own __eq__ (isinstance) accepts it
+    assert not r.storage.flags.writeable and np.shares_memory(r.storage, flat)
+    o = result_like(ours, 2, 3, np.arange(6, dtype=np.float64), tsm.Precision.DOUBLE)
+    assert type(o) is tsm.Matrix and o == ours
+
+
+def test_leading_dimension_rejects_overlapping_columns():
+    """gemm's stride check: expanded / stride-0 / overlapping column layouts raise."""
+    import torch
+
+    from paper_2002_03258_b200.kernels import _ld
+    base = torch.zeros(8, 64, dtype=torch.float64).t()  # 64 x 8 column-major, ld 64
+    assert _ld(base, 64) == 64
+    assert _ld(base[:40], 40) == 64  # row sub-view keeps the parent's ld
+    col = torch.zeros(64, 1, dtype=torch.float64)
+    assert _ld(col, 64) == 64  # one column: stride unused
+    expanded = torch.zeros(64, 1, dtype=torch.float64).expand(64, 8)  # stride (1, 0)
+    with pytest.raises(ValueError):
+        _ld(expanded, 64)
+    overlap = torch.zeros(200, dtype=torch.float64).as_strided((64, 4), (1, 16))
+    with pytest.raises(ValueError):
+        _ld(overlap, 64)
+    with pytest.raises(ValueError):
+        _ld(torch.zeros(64, 8, dtype=torch.float64), 64)  # row-major

@@ -11,7 +11,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2002_03258_b200.multi import gather_c, row_partition, run_sharded
+from paper_2002_03258_b200.multi import RowShards, colmajor_buffer, gather_c, row_partition, run_sharded
 
 
 def test_row_partition_covers_exactly():
@@ -67,4 +67,53 @@ def test_sharded_equals_whole(tmp_path, m, k, n, c_is_zero):
     got = np.load(out)
     C0 = np.zeros((m, n)) if c_is_zero else uniform_block(range(m), range(n), 3)
     whole = naive_gemm(uniform_block(range(m), range(k), 1), uniform_block(range(k), range(n), 2), C0)
+    assert np.array_equal(got, whole)
+
+
+def test_row_shards_modes():
+    for world in (1, 2, 3, 8):
+        strong = [RowShards("strong", world, r, m_total=65536) for r in range(world)]
+        assert sum(s.rows for s in strong) == 65536 and strong[0].r0 == 0 and strong[-1].r1 == 65536
+        weak = [RowShards("weak", world, r, rows_per_rank=30720) for r in range(world)]
+        assert all(s.rows == 30720 and s.m_total == 30720 * world for s in weak)
+    with pytest.raises(ValueError):
+        RowShards("diagonal", 2, 0, m_total=10)
+
+
+def _strong_worker(rank, world, port, m, k, n, steps, out_path):
+    """bench.py's strong-scaling step on CPU: RowShards split, B broadcast into a reused buffer
+    every step, local compute, gather."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.rng import uniform_block
+        sh = RowShards("strong", world, rank, m_total=m)
+        A = torch.from_numpy(uniform_block(range(sh.r0, sh.r1), range(k), 1)).t().contiguous().t()
+        C = torch.from_numpy(uniform_block(range(sh.r0, sh.r1), range(n), 3)).t().contiguous().t()
+        B = torch.from_numpy(uniform_block(range(k), range(n), 2)).t().contiguous().t() if rank == 0 else None
+        bbuf = colmajor_buffer(k, n, torch.float64, "cpu")
+        for _ in range(steps):  # C accumulates steps x A*B (C += A*B each step)
+            C, Bl = run_sharded(A, B, C, k=k, n=n, compute=_oracle_compute, b_out=bbuf)
+            assert Bl.data_ptr() == bbuf.data_ptr()
+        full = gather_c(C, m, n)
+        if rank == 0:
+            np.save(out_path, full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,m", [(2, 1000), (3, 1000), (3, 4133)])
+def test_strong_split_equals_whole(tmp_path, world, m):
+    """Uneven strong splits (ragged last shard, world 2 and 3) are bitwise the whole-matrix rows."""
+    from oracle import naive_gemm
+    from oracle.rng import uniform_block
+    k, n, steps = 96, 8, 2
+    out = str(tmp_path / "c.npy")
+    mp.start_processes(_strong_worker, args=(world, _free_port(), m, k, n, steps, out), nprocs=world, join=True,
+                       start_method="spawn")
+    got = np.load(out)
+    A, B = uniform_block(range(m), range(k), 1), uniform_block(range(k), range(n), 2)
+    whole = uniform_block(range(m), range(n), 3)
+    for _ in range(steps):
+        whole = naive_gemm(A, B, whole)
     assert np.array_equal(got, whole)

@@ -427,6 +427,71 @@ def test_config4_fp32_sampled():
         _check(Ch[r0:r0 + 128], ref, k, "single", what=r0)
 
 
+@pytest.mark.slow
+def test_config4_fp32_benchmarked_path_full():
+    """BASELINE config 4 exactly as benchmarked (fp32 32768^2 x 16, C += A*B with a nonzero C; the
+    split-precision tf32 tcgen05 path with fp64 split-row-block combine): the FULL result against
+    an fp64 cuBLAS product of the same device inputs (relative Frobenius <= 1e-5, and the max
+    relative error bound), plus 8 row slabs spread over the split row blocks against the oracle."""
+    import torch
+    from oracle.rng import uniform_block
+    tsm = _tsm()
+    m = k = 32768
+    n = 16
+    A = tsm.colmajor_empty(m, k, torch.float32, "cuda")
+    tsm.fill_uniform(A, seed=41)
+    B = tsm.colmajor_empty(k, n, torch.float32, "cuda")
+    tsm.fill_uniform(B, seed=42)
+    C = tsm.colmajor_empty(m, n, torch.float32, "cuda")
+    tsm.fill_uniform(C, seed=43)
+    C0 = C.clone()
+    from paper_2002_03258_b200 import tuning
+    plan = tuning.plan("single", m, k, n)
+    assert plan["consumer"] == "tc" and plan["nbig"] + plan["nsmall"] > 1  # split row blocks, tcgen05
+    tsm.gemm(A, B, C)
+    torch.cuda.synchronize()
+    Ch = C.cpu().numpy()
+    full = (C0.double() + A.double() @ B.double()).cpu().numpy()
+    assert rel_frobenius(Ch, full) <= 1e-5
+    assert max_rel_error(Ch, full) <= 8 * k * np.finfo(np.float32).eps
+    assert np.isfinite(Ch).all()
+    del A
+    torch.cuda.empty_cache()
+    Bh = uniform_block(range(k), range(n), 42, np.float32)
+    C0h = C0.cpu().numpy()
+    for r0 in np.linspace(0, m - 64, 8).astype(int):
+        rows = range(int(r0), int(r0) + 64)
+        ref = naive_gemm(uniform_block(rows, range(k), 41, np.float32), Bh, C0h[r0:r0 + 64])
+        _check(Ch[r0:r0 + 64], ref, k, "single", what=("config4 slab", int(r0)))
+
+
+@pytest.mark.slow
+def test_config3_l_opt2_zero_c_benchmarked_path():
+    """BASELINE config 3 as benchmarked: L_OPT2 (zero-C contract, C never read) at m = 2^24,
+    k = n = 16, fp64 — full result against cuBLAS DGEMM of the same inputs and sampled slabs
+    against the oracle. C starts as NaN so a read of C would show."""
+    import torch
+    from oracle.rng import uniform_block
+    tsm = _tsm()
+    m, k, n = 1 << 24, 16, 16
+    A = tsm.colmajor_empty(m, k, torch.float64, "cuda")
+    tsm.fill_uniform(A, seed=17)
+    B = tsm.colmajor_empty(k, n, torch.float64, "cuda")
+    tsm.fill_uniform(B, seed=18)
+    C = tsm.colmajor_empty(m, n, torch.float64, "cuda")
+    C.fill_(float("nan"))  # c_is_zero: the kernel must not read it
+    tsm.gemm(A, B, C, variant="l-opt2", c_is_zero=True)
+    torch.cuda.synchronize()
+    full = A @ B
+    assert torch.isfinite(C).all()
+    assert rel_frobenius(C.cpu().numpy(), full.cpu().numpy()) <= 1e-12
+    Bh = uniform_block(range(k), range(n), 18)
+    for r0 in (0, 5_000_017, m - 777):
+        rows = range(r0, min(m, r0 + 777))
+        ref = naive_gemm(uniform_block(rows, range(k), 17), Bh, np.zeros((len(rows), n)))
+        _check(C[r0:r0 + len(rows)].cpu().numpy(), ref, k, "double", what=("l-opt2", r0))
+
+
 @pytest.mark.parametrize("consumer", ["fma", "dmma", "ffma2", "tc", "dmmap", "dmma/cw16", "fma/cw16", "auto/sb64",
                                       "dmma/sb64"])
 def test_consumer_policies_subprocess(consumer):
