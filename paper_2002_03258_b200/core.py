@@ -118,6 +118,27 @@ class Variant(enum.Enum):
         return self in (Variant.L_OPT1, Variant.L_OPT2)
 
 
+_PAR_COPY_BYTES = 64 << 20
+
+
+def _copy_flat(storage, dtype) -> np.ndarray:
+    """A private flat copy of ``storage`` (the reference's Matrix copies its input, core.py:101).
+    Large contiguous arrays are copied in parallel slices (numpy releases the GIL in copyto), so
+    building a 7.5 GB Matrix is bound by memory bandwidth rather than one core."""
+    src = np.asarray(storage)
+    if src.dtype != dtype or src.nbytes < _PAR_COPY_BYTES or not src.flags.c_contiguous:
+        return np.array(src, dtype=dtype, copy=True).reshape(-1)
+    src = src.reshape(-1)
+    out = np.empty(src.size, dtype=dtype)
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    nt = max(1, min(8, os.cpu_count() or 1))
+    cuts = [src.size * i // nt for i in range(nt + 1)]
+    with ThreadPoolExecutor(nt) as pool:
+        list(pool.map(lambda i: np.copyto(out[cuts[i]:cuts[i + 1]], src[cuts[i]:cuts[i + 1]]), range(nt)))
+    return out
+
+
 class Matrix:
     """Dense column-major matrix over a frozen flat numpy array (element (i, j) at i + j*rows)."""
 
@@ -127,7 +148,7 @@ class Matrix:
         precision = Precision.coerce(precision)
         if rows < 1 or cols < 1:
             raise ValueError(f"matrix dimensions must be positive, got {rows}x{cols}")
-        flat = np.array(storage, dtype=precision.dtype, copy=True).reshape(-1)
+        flat = _copy_flat(storage, precision.dtype)
         if flat.size != rows * cols:
             raise ValueError(f"storage length {flat.size} != rows*cols = {rows * cols}")
         flat.flags.writeable = False

@@ -1347,7 +1347,9 @@ static int run_host_t(int variant, int64_t m, int64_t k, int64_t n, const T* A, 
   TSM2X_CUDA(cudaEventRecord(b_ready, hc->h2d));
   TSM2X_CUDA(cudaStreamWaitEvent(hc->comp, b_ready, 0));
 
-  const size_t slab_target = (size_t)256 << 20;
+  // pinned sources: 256 MB slabs (few, long DMAs); pageable: 32 MB, so the host threads' copy of
+  // slab j+1 into pinned staging overlaps the DMA of slab j even for a 134 MB A
+  const size_t slab_target = pinnedA ? (size_t)256 << 20 : (size_t)32 << 20;
   if (!use_l) {
     // ---- TSM2R: column slabs of A stream in while earlier slabs are multiplied; C stays on
     // the device (C += A[:, slab] * B[slab, :] per slab)

@@ -29,6 +29,19 @@ KEYS = [
     "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
     "launch__grid_size", "launch__block_size",
 ]
+# pipe / throughput metrics whose exact names vary between ncu versions and chips: every raw column
+# matching one of these patterns is recorded (the DMMA/HMMA tensor subpipes carry the fp64/fp32
+# tensor-core load; DRAM throughput is reported as dram__ or gpu__dram_ depending on the version)
+PATTERNS = [
+    r"^(gpu__)?dram__throughput\.avg\.pct_of_peak_sustained_elapsed$",
+    r"^gpu__dram_throughput\.avg\.pct_of_peak_sustained_elapsed$",
+    r"^dram__bytes\.sum\.per_second$",
+    r"^sm__pipe_tensor_subpipe_(dmma|hmma)_cycles_active\.avg\.pct_of_peak_sustained_(active|elapsed)$",
+    r"^sm__pipe_(tensor|fp64|shared)_cycles_active\.avg\.pct_of_peak_sustained_(active|elapsed)$",
+    r"^sm__inst_executed_pipe_(fp64|fma|lsu|uniform|tensor).*\.avg\.pct_of_peak_sustained_active$",
+    r"^l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld\.sum$",
+    r"^l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld\.sum$",
+]
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-9, "us": 1e-6,
               "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1, "nsecond": 1e-9, "Ghz": 1e9, "Mhz": 1e6,
               "hz": 1}
@@ -62,6 +75,9 @@ def summarise(report):
         e = {"kernel": row[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"}
         for k in KEYS:
             e[k] = value(hdr, units, row, k)
+        for name in hdr:
+            if name not in e and any(re.match(p, name) for p in PATTERNS):
+                e[name] = value(hdr, units, row, name)
         stalls = {}
         for i, name in enumerate(hdr):
             m = re.match(r"smsp__pcsamp_warps_issue_stalled_([a-z_]+)$", name)
