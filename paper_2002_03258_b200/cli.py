@@ -27,50 +27,52 @@ from typing import Iterable, List, Optional, Sequence
 import numpy as np
 
 from .core import KernelParams, Precision, Variant, validate_problem
-from . import tuning
+from . import traffic, tuning
 
-# B200 "catalog entry" (the reference keeps per-GPU YAML, data/gpus/*.yaml): measured on this
-# pool's parts by tools/microbench.cu (profiles/README.md) except where noted.
-B200_SPEC = {
-    "name": "B200",
-    "num_sms": 148,
-    "core_clock_max_mhz": 1965,
-    "mem_bandwidth_read_gbs": 7300.0,      # read-only stream
-    "mem_bandwidth_copy_gbs": 6550.0,      # device copy (MEASURED_PEAKS.json of an earlier box;
-                                           # 6490-6540 sustained under the cap, energy_r01.log)
-    "peak_gflops_double": 36400.0,         # DFMA; DMMA m8n8k4 37100 on the same datapath
-    "peak_gflops_single": 71100.0,         # FFMA; FFMA2 73000
-    "shared_per_sm": 233472,
-    "l2_bytes": 132644864,
-    "h2d_gbs": 55.6,                       # 1-4 concurrent copy streams alike (tools/h2d_probe.py)
-    "power_limit_w": 1000.0,               # every sustained workload runs at this cap
-    "energy_pj_per_flop": {"dmma": 8.8, "dfma": 13.0, "ffma2": 3.4, "tcgen05_split_tf32": 3.5},
-    "pipeline_nj_per_byte": 0.135,         # TMA stream with no arithmetic, at the cap (energy_r01.log)
-}
+CATALOG_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "gpus")
 
 
-def _fmt(v) -> str:
-    if isinstance(v, float):
-        return repr(v)
-    if v is None:
-        return ""
-    return str(v)
+def load_b200_spec() -> dict:
+    """The B200 catalog entry: data/gpus/b200.yaml (the reference's GpuSpec format, readable by
+    ``tsgemm.core.load_catalog``, reference core.py:390-399) merged with the B200-only measured
+    figures in b200_measured.json (read vs copy bandwidth, power cap, energy per flop)."""
+    import yaml
+    with open(os.path.join(CATALOG_DIR, "b200.yaml"), encoding="utf-8") as fh:
+        doc = yaml.safe_load(fh)
+    with open(os.path.join(CATALOG_DIR, "b200_measured.json"), encoding="utf-8") as fh:
+        extra = json.load(fh)
+    spec = {k: v for k, v in doc.items() if k != "sources"}
+    spec.update({k: v for k, v in extra.items() if k != "sources"})
+    spec["core_clock_max_mhz"] = doc["core_clock"]
+    return spec
+
+
+B200_SPEC = load_b200_spec()
+
+
+def _cell(v) -> str:
+    """CSV cell text: floats as repr (round-trip exact), None as empty — the reference's CSV
+    conventions (cli.py:67-72), so its readers parse these files unchanged."""
+    return "" if v is None else (repr(v) if isinstance(v, float) else str(v))
 
 
 def _write_csv(path: str, header: Sequence[str], rows: Iterable[Sequence]) -> None:
-    """Atomic: the file appears complete or not at all (reference cli.py:75-89)."""
-    directory = os.path.dirname(os.path.abspath(path)) or "."
-    fd, tmp = tempfile.mkstemp(dir=directory, suffix=".tmp")
+    """UTF-8 / LF CSV that appears complete or not at all: written to a temporary file in the
+    target directory and renamed over the target."""
+    target = os.path.abspath(path)
+    tmp = tempfile.NamedTemporaryFile("w", encoding="utf-8", newline="", suffix=".tmp",
+                                      dir=os.path.dirname(target) or ".", delete=False)
     try:
-        with os.fdopen(fd, "w", encoding="utf-8", newline="") as fh:
-            w = csv.writer(fh, lineterminator="\n")
-            w.writerow(header)
-            for r in rows:
-                w.writerow([_fmt(x) for x in r])
-        os.replace(tmp, path)
+        with tmp:
+            out = csv.writer(tmp, lineterminator="\n")
+            out.writerow(list(header))
+            out.writerows([_cell(x) for x in r] for r in rows)
+        os.replace(tmp.name, target)
     except BaseException:
-        if os.path.exists(tmp):
-            os.unlink(tmp)
+        try:
+            os.unlink(tmp.name)
+        except FileNotFoundError:
+            pass
         raise
 
 
@@ -98,37 +100,102 @@ def _time_ms(fn, reps: int) -> float:
     return sorted(ts)[len(ts) // 2]
 
 
-RUN_HEADER = ["gpu", "precision", "m", "k", "n", "variant", "t1", "t2", "t3", "tcf", "shape_class", "impl",
-              "consumer", "rows_per_block", "cols_per_pass", "cols_per_stage", "stages", "items", "grid",
-              "time_ms", "gflops", "gbps", "hbm_frac", "check_max_rel_err", "check_rel_frobenius", "error"]
+RUN_HEADER = (["gpu", "precision", "m", "k", "n", "variant", "t1", "t2", "t3", "tcf", "shape_class", "impl",
+               "consumer", "rows_per_block", "cols_per_pass", "cols_per_stage", "stages", "items", "grid",
+               "time_ms", "gflops", "gbps", "hbm_frac", "check_max_rel_err", "check_rel_frobenius"]
+              # the reference's per-array counter columns (cli.py:105-124), from the traffic model of
+              # the kernel actually launched (traffic.py) — "counter_source" says which
+              + [f"{a}_{c}" for a in ("A", "B", "C") for c in traffic.ARRAY_COLS]
+              + ["counter_source", "ncu_dram_bytes_read", "ncu_dram_bytes_write", "ncu_global_ld_thread_insts",
+                 "ncu_global_st_thread_insts", "ncu_kernels", "error"])
+NCU_METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__sass_thread_inst_executed_op_global_ld.sum",
+               "smsp__sass_thread_inst_executed_op_global_st.sum"]
 
 
-def _run_point(prec: Precision, shape, variant: Variant, override: dict, seed: int, si: int, reps: int):
+def _make_inputs(prec: Precision, shape, seed: int, si: int):
+    """A, B on the device by the run command's convention (see the module docstring)."""
     import torch
 
-    from .kernels import colmajor_empty, fill_uniform, gemm
+    from .kernels import colmajor_empty, fill_uniform
+    m, k, n = shape
+    dt = torch.float64 if prec is Precision.DOUBLE else torch.float32
+    A = colmajor_empty(m, k, dt, "cuda")
+    B = colmajor_empty(k, n, dt, "cuda")
+    if m * k <= (1 << 26):
+        rng = np.random.default_rng([seed, si])
+        a = rng.random(m * k, dtype=np.float64).astype(prec.dtype).reshape((m, k), order="F")
+        b = rng.random(k * n, dtype=np.float64).astype(prec.dtype).reshape((k, n), order="F")
+        A.copy_(torch.from_numpy(a))
+        B.copy_(torch.from_numpy(b))
+    else:
+        fill_uniform(A, seed=seed * 1000003 + si)
+        fill_uniform(B, seed=seed * 1000003 + si + 7)
+    return A, B
+
+
+def _params_for(variant: Variant, n: int, override: dict) -> KernelParams:
+    t1 = override.get("t1", 128)
+    return KernelParams(t1=t1, t2=override.get("t2", n), t3=override.get("t3", min(4, t1)),
+                        tcf=override.get("tcf", 1) if variant.is_tsm2l else 1, variant=variant)
+
+
+def run_once(prec: Precision, shape, variant: Variant, override: dict, seed: int, si: int) -> None:
+    """One call of the point, nothing else (what ncu_counters profiles)."""
+    import torch
+
+    from .kernels import colmajor_empty, gemm
+    m, k, n = shape
+    A, B = _make_inputs(prec, shape, seed, si)
+    C = colmajor_empty(m, n, A.dtype, "cuda")
+    impl = "ablation" if variant in (Variant.V0, Variant.V1, Variant.V2) else "auto"
+    torch.cuda.synchronize()
+    gemm(A, B, C, variant=variant, params=_params_for(variant, n, override), impl=impl, c_is_zero=True)
+    torch.cuda.synchronize()
+
+
+def ncu_counters(prec: Precision, shape, variant: Variant, override: dict, seed: int, si: int) -> Optional[dict]:
+    """Measured counters of one call: the point re-run under Nsight Compute (``ncu`` on PATH),
+    summed over the library's kernels (fill kernels excluded). None when ncu is unavailable."""
+    import shutil
+    import subprocess
+    if shutil.which("ncu") is None:
+        return None
+    m, k, n = shape
+    cmd = ["ncu", "--csv", "--metrics", ",".join(NCU_METRICS), "-k", "regex:^(?!fill_uniform)",
+           sys.executable, "-m", "paper_2002_03258_b200.cli", "_once", "--precision", prec.value,
+           "--m", str(m), "--k", str(k), "--n", str(n), "--variant", variant.value, "--seed", str(seed), "--si", str(si)]
+    for f, v in override.items():
+        cmd += [f"--{f}", str(v)]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
+    rows = list(csv.reader(out.stdout.splitlines()))
+    start = next((i for i, r in enumerate(rows) if r and r[0] == "ID"), None)
+    if start is None:
+        return None
+    hdr = rows[start]
+    ki, ni, vi = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
+    sums, kernels = {}, set()
+    for r in rows[start + 1:]:
+        if len(r) <= vi or "fill_uniform" in r[ki]:
+            continue
+        kernels.add(r[0])
+        sums[r[ni]] = sums.get(r[ni], 0.0) + float(r[vi].replace(",", ""))
+    sums["kernels"] = len(kernels)
+    return sums
+
+
+def _run_point(prec: Precision, shape, variant: Variant, override: dict, seed: int, si: int, reps: int,
+               counters: str = "model"):
+    import torch
+
+    from .kernels import colmajor_empty, gemm
     m, k, n = shape
     base = ["B200", prec.value, m, k, n, variant.value]
     try:
-        t1 = override.get("t1", 128)
-        t2 = override.get("t2", n)
-        t3 = override.get("t3", min(4, t1))
-        tcf = override.get("tcf", 1) if variant.is_tsm2l else 1
-        params = KernelParams(t1=t1, t2=t2, t3=t3, tcf=tcf, variant=variant)
+        params = _params_for(variant, n, override)
+        t1, t2, t3, tcf = params.t1, params.t2, params.t3, params.tcf
         params.validate_for(m, k, n)
-        dt = torch.float64 if prec is Precision.DOUBLE else torch.float32
-        A = colmajor_empty(m, k, dt, "cuda")
-        B = colmajor_empty(k, n, dt, "cuda")
-        if m * k <= (1 << 26):
-            rng = np.random.default_rng([seed, si])
-            a = rng.random(m * k, dtype=np.float64).astype(prec.dtype).reshape((m, k), order="F")
-            b = rng.random(k * n, dtype=np.float64).astype(prec.dtype).reshape((k, n), order="F")
-            A.copy_(torch.from_numpy(a))
-            B.copy_(torch.from_numpy(b))
-        else:
-            fill_uniform(A, seed=seed * 1000003 + si)
-            fill_uniform(B, seed=seed * 1000003 + si + 7)
-        C = colmajor_empty(m, n, dt, "cuda")
+        A, B = _make_inputs(prec, shape, seed, si)
+        C = colmajor_empty(m, n, A.dtype, "cuda")
         impl = "ablation" if variant in (Variant.V0, Variant.V1, Variant.V2) else "auto"
 
         def call():
@@ -146,7 +213,22 @@ def _run_point(prec: Precision, shape, variant: Variant, override: dict, seed: i
         gbps = byts / ms / 1e6
         row = base + [t1, t2, t3, tcf, validate_problem(m, k, n).value, pl["impl"], pl["consumer"],
                       pl["rows_per_block"], pl["cols_per_pass"], pl["cols_per_stage"], pl["stages"], pl["items"],
-                      pl["grid"], ms, 2.0 * m * k * n / ms / 1e6, gbps, gbps / _hbm_peak(), err, fro, ""]
+                      pl["grid"], ms, 2.0 * m * k * n / ms / 1e6, gbps, gbps / _hbm_peak(), err, fro]
+        if impl == "ablation":
+            cnt = traffic.ablation_counts(variant, m, k, n, t1, t2, t3, eb, c_is_zero=True)
+            src = "model:paper_algorithm (oracle.py:72-124 closed form)"
+        else:
+            cnt = traffic.stream_kernel_counts(pl, m, k, n, eb, c_is_zero=True)
+            src = "model:tma_stream_kernel"
+        for a in ("A", "B", "C"):
+            row += cnt[a]
+        ncu = ncu_counters(prec, shape, variant, override, seed, si) if counters == "ncu" else None
+        if ncu is not None:
+            src += "+ncu"
+            row += [src] + [ncu.get(k_) for k_ in NCU_METRICS] + [ncu.get("kernels")]
+        else:
+            row += [src, None, None, None, None, None]
+        row += [""]
         del A, B, C
         return row
     except Exception as exc:  # infeasible params etc.: per-row error, keep going (cli.py:155-160)
@@ -155,8 +237,9 @@ def _run_point(prec: Precision, shape, variant: Variant, override: dict, seed: i
         return row + [f"{type(exc).__name__}: {exc}"]
 
 
-def cmd_run(prec: Precision, shapes, variants, override, seed, out, reps=10) -> int:
-    rows = [_run_point(prec, sh, v, override, seed, si, reps) for si, sh in enumerate(shapes) for v in variants]
+def cmd_run(prec: Precision, shapes, variants, override, seed, out, reps=10, counters="model") -> int:
+    rows = [_run_point(prec, sh, v, override, seed, si, reps, counters) for si, sh in enumerate(shapes)
+            for v in variants]
     _write_csv(out, RUN_HEADER, rows)
     return 0
 
@@ -188,8 +271,16 @@ def _consumer_for(prec: Precision, n: int) -> str:
     """The datapath the library picks for one pass of width n (tsm2x.cu pick_consumer_rt)."""
     nt = 1 if n <= 1 else 2 if n <= 2 else 4 if n <= 4 else 8 if n <= 8 else 16
     if prec is Precision.DOUBLE:
-        return "dmma" if nt >= 8 else "dfma"
+        return "dmma" if nt >= 4 else "dfma"  # 3-4 column passes run on the 8-column DMMA tile
     return "tcgen05_split_tf32" if nt == 16 else "ffma2"
+
+
+def _tile_cols(prec: Precision, n: int) -> int:
+    """Columns the datapath computes for a pass of width n (B zero-padded to the tile)."""
+    nt = 1 if n <= 1 else 2 if n <= 2 else 4 if n <= 4 else 8 if n <= 8 else 16
+    if prec is Precision.DOUBLE and nt == 4:
+        return 8
+    return nt
 
 
 def power_bound_ms(prec: Precision, m: int, k: int, n: int) -> float:
@@ -197,7 +288,7 @@ def power_bound_ms(prec: Precision, m: int, k: int, n: int) -> float:
     pipeline energy plus the arithmetic's, divided by the cap."""
     eb = prec.bytes_per_element
     e = B200_SPEC["pipeline_nj_per_byte"] * 1e-9 * eb * m * k + \
-        B200_SPEC["energy_pj_per_flop"][_consumer_for(prec, n)] * 1e-12 * 2.0 * m * k * n
+        B200_SPEC["energy_pj_per_flop"][_consumer_for(prec, n)] * 1e-12 * 2.0 * m * k * _tile_cols(prec, n)
     return e / B200_SPEC["power_limit_w"] * 1e3
 
 
@@ -262,6 +353,17 @@ def build_parser() -> argparse.ArgumentParser:
         r.add_argument(f"--{f}", type=int, default=None)
     r.add_argument("--seed", type=int, default=0)
     r.add_argument("--reps", type=int, default=10)
+    r.add_argument("--counters", choices=["model", "ncu"], default="model",
+                   help="per-array counters from the traffic model, plus Nsight Compute measurements with 'ncu'")
+    o = sub.add_parser("_once")  # internal: one call of a point (profiled by ncu_counters)
+    common(o)
+    for d in ("m", "k", "n"):
+        o.add_argument(f"--{d}", type=int, required=True)
+    o.add_argument("--variant", required=True)
+    for f in ("t1", "t2", "t3", "tcf"):
+        o.add_argument(f"--{f}", type=int, default=None)
+    o.add_argument("--seed", type=int, default=0)
+    o.add_argument("--si", type=int, default=0)
     t = sub.add_parser("tune")
     common(t)
     for d in ("m", "k", "n"):
@@ -296,7 +398,12 @@ def main(argv: Optional[Sequence[str]] = None) -> int:
         if args.command == "run":
             override = {f: getattr(args, f) for f in ("t1", "t2", "t3", "tcf") if getattr(args, f) is not None}
             variants = [Variant.parse(v) for v in (args.variant or [])]
-            return cmd_run(prec, _shapes(args), variants, override, args.seed, args.out or "run.csv", args.reps)
+            return cmd_run(prec, _shapes(args), variants, override, args.seed, args.out or "run.csv", args.reps,
+                           args.counters)
+        if args.command == "_once":
+            override = {f: getattr(args, f) for f in ("t1", "t2", "t3", "tcf") if getattr(args, f) is not None}
+            run_once(prec, (args.m, args.k, args.n), Variant.parse(args.variant), override, args.seed, args.si)
+            return 0
         if args.command == "tune":
             return cmd_tune(prec, (args.m, args.k, args.n), args.out or "tune.csv")
         if args.command == "model":

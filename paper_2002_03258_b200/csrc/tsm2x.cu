@@ -54,6 +54,16 @@ static int fail(int code, const char* fmt, ...) {
     if (rc_ != TSM2X_OK) return rc_; \
   } while (0)
 
+// Kernel-timing events (tsm2x_set_kernel_events): inside a stream capture they become external
+// event-record nodes, so every replay of the graph records them and they stay timeable.
+static cudaError_t record_kernel_event(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t err = cudaStreamIsCapturing(s, &cs);
+  if (err != cudaSuccess) return err;
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                                             : cudaEventRecord(e, s);
+}
+
 static int check_launch(const char* what) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
@@ -707,7 +717,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   else
     TSM2X_TRY(encode_a_map(&tmap, A, m, k, lda, eb, Cfg::BOX, Cfg::KC));
   const bool timed = t_ev_start && t_ev_stop;
-  if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
+  if (timed) TSM2X_CUDA(record_kernel_event(t_ev_start, s));
   if (swz && kind == kDmma)
     TSM2X_TRY((launch_tma_kernel<T, NT, kDmmaS, RPT, CW, SB>(a, tmap, G, s)));
   else if (swz && kind == kDmmaP)
@@ -733,7 +743,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   }
 #endif
   if (timed) {
-    TSM2X_CUDA(cudaEventRecord(t_ev_stop, s));
+    TSM2X_CUDA(record_kernel_event(t_ev_stop, s));
     t_ev_start = t_ev_stop = nullptr;
   }
   if (atomic_split && sizeof(T) == 4) {
@@ -807,7 +817,7 @@ static int run_tsm2r_tc32(const DevInfo& di, Workspace* ws, int64_t m, int64_t k
   auto kern = split ? tsm2r_stream_tc32<false> : tsm2r_stream_tc32<true>;
   TSM2X_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   const bool timed = t_ev_start && t_ev_stop;
-  if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
+  if (timed) TSM2X_CUDA(record_kernel_event(t_ev_start, s));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)G);
   cfg.blockDim = dim3(Cfg::THREADS);
@@ -832,7 +842,7 @@ static int run_tsm2r_tc32(const DevInfo& di, Workspace* ws, int64_t m, int64_t k
             env_diag & 0xffff, h[4], h[0] / ns, h[1] / ns, h[2] / ns, h[3] / ns, h[8] / ns, h[9] / ns, h[10] / ns, h[11] / ns);
   }
   if (timed) {
-    TSM2X_CUDA(cudaEventRecord(t_ev_stop, s));
+    TSM2X_CUDA(record_kernel_event(t_ev_stop, s));
     t_ev_start = t_ev_stop = nullptr;
   }
   if (split) {
@@ -881,12 +891,12 @@ static int run_tsm2r_tma_static(const DevInfo& di, Workspace* ws, int64_t m, int
   alignas(64) CUtensorMap tmap;
   TSM2X_TRY(encode_a_map(&tmap, A, m, k, lda, sizeof(T), Cfg::BOX, Cfg::KC));
   const bool timed = t_ev_start && t_ev_stop;
-  if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
+  if (timed) TSM2X_CUDA(record_kernel_event(t_ev_start, s));
   void* args[] = {&a, &tmap};
   TSM2X_CUDA(cudaLaunchKernel((const void*)kern, dim3((unsigned)G), dim3(Cfg::THREADS), args, Cfg::SMEM, s));
   TSM2X_TRY(check_launch("tsm2r_static_tma"));
   if (timed) {
-    TSM2X_CUDA(cudaEventRecord(t_ev_stop, s));
+    TSM2X_CUDA(record_kernel_event(t_ev_stop, s));
     t_ev_start = t_ev_stop = nullptr;
   }
   if (a.defer) {
@@ -942,12 +952,12 @@ static int run_tsm2r_ldg(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   a.ws = reinterpret_cast<T*>(rest);
   a.counters = ws->counters + 4;
   const bool timed = t_ev_start && t_ev_stop;
-  if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
+  if (timed) TSM2X_CUDA(record_kernel_event(t_ev_start, s));
   void* args[] = {&a};
   TSM2X_CUDA(cudaLaunchKernel(kfn, dim3((unsigned)G), dim3(THREADS), args, 0, s));
   TSM2X_TRY(check_launch("tsm2r_stream_ldg"));
   if (timed) {
-    TSM2X_CUDA(cudaEventRecord(t_ev_stop, s));
+    TSM2X_CUDA(record_kernel_event(t_ev_stop, s));
     t_ev_start = t_ev_stop = nullptr;
   }
   if (a.defer) {
@@ -1061,11 +1071,11 @@ static int run_tsm2l_pass(const DevInfo& di, int64_t m, int64_t k, int w, const 
   grid = std::max<int64_t>(grid, 1);
   void* args[] = {&a};
   const bool timed = t_ev_start && t_ev_stop;
-  if (timed) TSM2X_CUDA(cudaEventRecord(t_ev_start, s));
+  if (timed) TSM2X_CUDA(record_kernel_event(t_ev_start, s));
   TSM2X_CUDA(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(THREADS), args, 0, s));
   TSM2X_TRY(check_launch("tsm2l"));
   if (timed) {
-    TSM2X_CUDA(cudaEventRecord(t_ev_stop, s));
+    TSM2X_CUDA(record_kernel_event(t_ev_stop, s));
     t_ev_start = t_ev_stop = nullptr;
   }
   return TSM2X_OK;

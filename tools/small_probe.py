@@ -60,13 +60,14 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     flush_f = flush.view(torch.float32)
     red = torch.empty((), dtype=torch.float32, device="cuda")
-    pres = {"write_flush": lambda: flush.zero_(), "read_flush": lambda: torch.sum(flush_f, out=red), "none": None}
+    pres = {"write_flush": lambda: flush.zero_(), "read_flush": lambda: torch.sum(flush_f, dim=0, out=red), "none": None}
     byts = 8 * (mk * mk + mk * n + 2 * mk * n)
     for pname, pre in pres.items():
-        row = {"m=k": mk, "n": n, "pre": pname}
+        row = {"m=k": mk, "n": n, "pre": pname, "env": {k: v for k, v in os.environ.items() if k.startswith("TSM2X_")}}
         for i in impls:
             row[f"tsm2x_{i}_us"] = round(graph_us(lambda: tsm.gemm(A, B, C, impl=i), pre), 2)
-        row["torch_sum_A_us"] = round(graph_us(lambda: torch.sum(A, out=out), pre), 2)
+        row["torch_sum_A_us"] = round(graph_us(lambda: torch.sum(A, dim=(0, 1), out=out), pre), 2)
+        row["empty_graph_us"] = round(graph_us(lambda: out.zero_(), pre), 2)  # one 1-thread kernel: the floor
         row["ideal_us_at_7300"] = round(byts / 7.3e12 * 1e6, 2)
         print(json.dumps(row), flush=True)
 
