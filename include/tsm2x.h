@@ -74,7 +74,9 @@ enum tsm2x_impl {
   TSM2X_IMPL_STREAM_LDG = 1,  /* TSM2R: register-prefetched LDG.128 stream, stream-K split  */
   TSM2X_IMPL_STREAM_TMA = 2,  /* TSM2R: bulk-copy (TMA engine) smem ring, warp-specialised  */
   TSM2X_IMPL_TSM2L = 3,       /* TSM2L: whole B in smem, grid-stride row stream              */
-  TSM2X_IMPL_ABLATION = 4     /* the paper's V0/V1/V2 algorithms as written (ablation only)  */
+  TSM2X_IMPL_ABLATION = 4,    /* the paper's V0/V1/V2 algorithms as written (ablation only)  */
+  TSM2X_IMPL_TSM2L_SPLITN = 5 /* TSM2L split-n: 4 lanes per row group, warp-shuffle combine
+                                 (A/B candidate, k <= 64; profiles/splitn_r02.json)           */
 };
 
 /* Validation only (no device work): mirrors the reference's ValueError conditions. */

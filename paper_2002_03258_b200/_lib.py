@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("TSM2X_LIB_PATH_EXPERIMENT") or os.path.join(_HERE, "l
 
 OK, EINVAL, ECUDA, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4
 FLAG_C_IS_ZERO, FLAG_CHECK_ZERO_C, FLAG_DETERMINISTIC = 0x1, 0x2, 0x4
-IMPL = {"auto": 0, "ldg": 1, "tma": 2, "tsm2l": 3, "ablation": 4}
+IMPL = {"auto": 0, "ldg": 1, "tma": 2, "tsm2l": 3, "ablation": 4, "tsm2l-splitn": 5}
 SINGLE, DOUBLE = 0, 1
 
 EXPORTS = (

@@ -108,8 +108,10 @@ RUN_HEADER = (["gpu", "precision", "m", "k", "n", "variant", "t1", "t2", "t3", "
               + [f"{a}_{c}" for a in ("A", "B", "C") for c in traffic.ARRAY_COLS]
               + ["counter_source", "ncu_dram_bytes_read", "ncu_dram_bytes_write", "ncu_global_ld_thread_insts",
                  "ncu_global_st_thread_insts", "ncu_kernels", "error"])
-NCU_METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__sass_thread_inst_executed_op_global_ld.sum",
-               "smsp__sass_thread_inst_executed_op_global_st.sum"]
+# ncu counts warp-level LDG/STG instructions; the thread-level columns are those x 32 (every lane
+# of the ablation kernels' warps is active at the 32-row-multiple shapes the CLI is run on)
+NCU_METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__sass_inst_executed_op_global_ld.sum",
+               "smsp__sass_inst_executed_op_global_st.sum"]
 
 
 def _make_inputs(prec: Precision, shape, seed: int, si: int):
@@ -178,7 +180,10 @@ def ncu_counters(prec: Precision, shape, variant: Variant, override: dict, seed:
         if len(r) <= vi or "fill_uniform" in r[ki]:
             continue
         kernels.add(r[0])
-        sums[r[ni]] = sums.get(r[ni], 0.0) + float(r[vi].replace(",", ""))
+        try:
+            sums[r[ni]] = sums.get(r[ni], 0.0) + float(r[vi].replace(",", ""))
+        except ValueError:  # "n/a": metric not collected for this kernel
+            pass
     sums["kernels"] = len(kernels)
     return sums
 
@@ -225,7 +230,9 @@ def _run_point(prec: Precision, shape, variant: Variant, override: dict, seed: i
         ncu = ncu_counters(prec, shape, variant, override, seed, si) if counters == "ncu" else None
         if ncu is not None:
             src += "+ncu"
-            row += [src] + [ncu.get(k_) for k_ in NCU_METRICS] + [ncu.get("kernels")]
+            vals = [ncu.get(k_) for k_ in NCU_METRICS]
+            vals[2:4] = [None if v_ is None else 32 * v_ for v_ in vals[2:4]]  # warp -> thread instructions
+            row += [src] + vals + [ncu.get("kernels")]
         else:
             row += [src, None, None, None, None, None]
         row += [""]

@@ -233,7 +233,9 @@ def result_like(C, rows: int, cols: int, flat: np.ndarray, precision: Precision)
     so ``==`` against reference results (whose ``__eq__`` checks ``isinstance``) keeps working.
     The freshly produced array is adopted without a copy either way."""
     cls = type(C)
-    if cls is Matrix or not all(hasattr(C, a) for a in Matrix.__slots__):
+    # only a Matrix class proper (the reference's: same __slots__ and methods) is mirrored; other
+    # duck-typed inputs get this package's Matrix
+    if cls is Matrix or tuple(getattr(cls, "__slots__", ())) != Matrix.__slots__ or not hasattr(cls, "to_2d"):
         return Matrix._adopt(rows, cols, flat, precision)
     obj = cls.__new__(cls)
     flat = flat.reshape(-1)

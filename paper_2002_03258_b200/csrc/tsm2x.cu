@@ -21,6 +21,7 @@
 #include "ablation.cuh"
 #include "common.cuh"
 #include "tsm2l.cuh"
+#include "tsm2l_splitn.cuh"
 #include "tsm2r_stream.cuh"
 #include "tsm2r_tma.cuh"
 #include "tsm2r_tma_static.cuh"
@@ -1081,6 +1082,45 @@ static int run_tsm2l_pass(const DevInfo& di, int64_t m, int64_t k, int w, const 
   return TSM2X_OK;
 }
 
+// TSM2L split-n (tsm2l_splitn.cuh): S lanes per row group, warp-shuffle combine. A/B candidate
+// (TSM2X_IMPL_TSM2L_SPLITN), never chosen automatically: profiles/splitn_r02.json.
+template <typename T, int NT>
+static int run_tsm2l_splitn_pass(const DevInfo& di, int64_t m, int64_t k, int w, const T* A, int64_t lda, const T* B,
+                                 int64_t ldb, T* C, int64_t ldc, bool c_is_zero, cudaStream_t s) {
+  if constexpr (NT < 4) {
+    return run_tsm2l_pass<T, NT>(di, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, s);  // too few columns to split
+  } else {
+    constexpr int THREADS = 256, S = 4, KCH = 4;
+    const bool vec = aligned16(A) && aligned16(C) && (lda % Vec<T>::N == 0) && (ldc % Vec<T>::N == 0);
+    if (!vec) return run_tsm2l_pass<T, NT>(di, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, s);
+    LArgs<T> a;
+    a.A = A;
+    a.lda = lda;
+    a.B = B;
+    a.ldb = ldb;
+    a.C = C;
+    a.ldc = ldc;
+    a.m = m;
+    a.k = (int)k;
+    a.w = w;
+    a.c_is_zero = c_is_zero ? 1 : 0;
+    auto kern = tsm2l_splitn_kernel<T, NT, S, THREADS, KCH>;
+    const int occ = occupancy(kern, THREADS, 0);
+    const int64_t groups = (m + Vec<T>::N - 1) / Vec<T>::N;
+    int64_t grid = std::min<int64_t>((groups + THREADS / S - 1) / (THREADS / S), (int64_t)di.sms * occ);
+    grid = std::max<int64_t>(grid, 1);
+    const bool timed = t_ev_start && t_ev_stop;
+    if (timed) TSM2X_CUDA(record_kernel_event(t_ev_start, s));
+    kern<<<(unsigned)grid, THREADS, 0, s>>>(a);
+    TSM2X_TRY(check_launch("tsm2l_splitn"));
+    if (timed) {
+      TSM2X_CUDA(record_kernel_event(t_ev_stop, s));
+      t_ev_start = t_ev_stop = nullptr;
+    }
+    return TSM2X_OK;
+  }
+}
+
 template <typename T>
 __global__ void nonzero_check(const T* __restrict__ C, int64_t m, int64_t n, int64_t ldc, int* flag) {
   int64_t tot = m * n;
@@ -1127,7 +1167,8 @@ static int run_device(int variant, int64_t m, int64_t k, int64_t n, const T* A, 
   // the TMA stream kernel also covers TSM2L shapes (single-chunk row blocks); the LDG TSM2L
   // kernel is the fallback for layouts TMA cannot describe, or on request
   const bool tma_layout = aligned16(A) && ((lda * (int64_t)sizeof(T)) % 16 == 0);
-  const bool use_l = (impl == TSM2X_IMPL_TSM2L) || (impl == TSM2X_IMPL_AUTO && k <= TSM2L_KMAX && !tma_layout);
+  const bool splitn = impl == TSM2X_IMPL_TSM2L_SPLITN;
+  const bool use_l = (impl == TSM2X_IMPL_TSM2L) || splitn || (impl == TSM2X_IMPL_AUTO && k <= TSM2L_KMAX && !tma_layout);
   if (use_l && k > TSM2L_KMAX) return fail(TSM2X_EINVAL, "TSM2L kernel needs k <= %d, got %lld", TSM2L_KMAX, (long long)k);
   for (int64_t p = 0; p < n; p += 16) {
     const int w = (int)std::min<int64_t>(16, n - p);
@@ -1140,7 +1181,8 @@ static int run_device(int variant, int64_t m, int64_t k, int64_t n, const T* A, 
     int rc;
 #define TSM2X_PASS(NTV)                                                                                     \
   case NTV:                                                                                                 \
-    rc = use_l ? run_tsm2l_pass<T, NTV>(di, m, k, w, A, lda, Bp, ldb, Cp, ldc, c_is_zero, s)                \
+    rc = splitn  ? run_tsm2l_splitn_pass<T, NTV>(di, m, k, w, A, lda, Bp, ldb, Cp, ldc, c_is_zero, s)        \
+         : use_l ? run_tsm2l_pass<T, NTV>(di, m, k, w, A, lda, Bp, ldb, Cp, ldc, c_is_zero, s)                \
                : run_tsm2r_pass<T, NTV>(di, ws, impl, m, k, w, A, lda, Bp, ldb, Cp, ldc, c_is_zero, determ, s); \
     break;
     switch (nt) {
@@ -1505,7 +1547,7 @@ int tsm2x_run_ex(int variant, int precision, int64_t m, int64_t k, int64_t n, co
                  const void* B, int64_t ldb, void* C, int64_t ldc, const tsm2x_params* params, uint32_t flags,
                  int impl, void* stream) {
   TSM2X_TRY(validate(variant, precision, m, k, n, params));
-  if (impl < TSM2X_IMPL_AUTO || impl > TSM2X_IMPL_ABLATION) return fail(TSM2X_EINVAL, "unknown impl %d", impl);
+  if (impl < TSM2X_IMPL_AUTO || impl > TSM2X_IMPL_TSM2L_SPLITN) return fail(TSM2X_EINVAL, "unknown impl %d", impl);
   return run_device_any(variant, precision, m, k, n, A, lda, B, ldb, C, ldc, params, flags, impl,
                         reinterpret_cast<cudaStream_t>(stream));
 }
@@ -1626,6 +1668,12 @@ int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, 
   cudaGetLastError();
   const bool tma_layout = a_aligned16 && ((lda * (int64_t)eb) % 16 == 0) && m < (int64_t(1) << 31);
   const bool determ = (flags & TSM2X_FLAG_DETERMINISTIC) != 0;
+  if (impl == TSM2X_IMPL_TSM2L_SPLITN) {
+    out->impl = TSM2X_IMPL_TSM2L_SPLITN;
+    out->rows_per_block = 256 / 4 * (int)(16 / eb);  // 64 row groups of one 16-byte vector per CTA
+    out->cols_per_pass = nt;
+    return TSM2X_OK;
+  }
   if (impl == TSM2X_IMPL_ABLATION || impl == TSM2X_IMPL_TSM2L ||
       (impl == TSM2X_IMPL_AUTO && k <= TSM2L_KMAX && !tma_layout)) {
     out->impl = impl == TSM2X_IMPL_ABLATION ? TSM2X_IMPL_ABLATION : TSM2X_IMPL_TSM2L;

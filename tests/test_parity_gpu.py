@@ -693,3 +693,31 @@ def test_cuda_graph_capture_and_replay():
             torch.cuda.synchronize()
             prec = "double" if dt == torch.float64 else "single"
             assert rel_frobenius(C.cpu().numpy(), ref) <= TOL_FROB[prec], (m, k, n, dt)
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+@pytest.mark.parametrize("m,k,n,c_zero", [(100003, 16, 16, True), (4099, 7, 8, False), (65536, 64, 4, False),
+                                         (333, 16, 5, True), (1, 3, 16, False)])
+def test_tsm2l_splitn_against_oracle(prec, m, k, n, c_zero):
+    """The split-n warp-shuffle TSM2L kernel (impl tsm2l-splitn): ragged m, k not a multiple of
+    the 4-way split, pass widths 4/8/16 and a ragged last pass, zero and nonzero C."""
+    import torch
+    from oracle.rng import uniform_block
+    tsm = _tsm()
+    dt = torch.float64 if prec == "double" else torch.float32
+    npdt = np.float64 if prec == "double" else np.float32
+    A = tsm.colmajor_empty(m, k, dt, "cuda")
+    tsm.fill_uniform(A, seed=61)
+    B = tsm.colmajor_empty(k, n, dt, "cuda")
+    tsm.fill_uniform(B, seed=62)
+    C = tsm.colmajor_empty(m, n, dt, "cuda")
+    if c_zero:
+        C.fill_(float("nan"))
+    else:
+        tsm.fill_uniform(C, seed=63)
+    C0h = np.zeros((m, n), npdt) if c_zero else C.cpu().numpy()
+    tsm.gemm(A, B, C, variant="l-opt2" if c_zero else "l-opt1", c_is_zero=c_zero, impl="tsm2l-splitn")
+    torch.cuda.synchronize()
+    ref = naive_gemm(uniform_block(range(m), range(k), 61).astype(npdt), uniform_block(range(k), range(n), 62).astype(npdt),
+                     C0h)
+    _check(C.cpu().numpy(), ref, k, prec, what=("splitn", m, k, n, c_zero))

@@ -8,7 +8,7 @@ paper_2002_03258_b200/traffic.py:paper_algorithm_loads) — SURVEY.md §8 row a1
 Cases: the paper's V0 (inner product), V1 (outer product, t2 columns per pass), V2 (+ shared B
 tile) at t2 = n and t2 < n, and the production V3 kernel. A is m x m fp64 (m = 8192: 537 MB, 4x
 the L2), so every pass over A is a DRAM pass and ncu's dram__bytes_read must be ~ eb x loads["A"]
-(+ B, C). Thread-level global load / store instructions (SASS counters) are compared with the
+(+ B, C). Global load / store instructions (SASS warp counters x 32 lanes) are compared with the
 oracle's per-element load / store totals. Writes profiles/traffic_<tag>.json.
 """
 
@@ -29,8 +29,8 @@ CASES = {  # name: (variant, t1, t2, t3, impl)
     "v2_t2_4": ("v2", 128, 4, 4, "ablation"),
     "v3_b200": ("v3", 128, None, 4, "auto"),
 }
-METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__sass_thread_inst_executed_op_global_ld.sum",
-           "smsp__sass_thread_inst_executed_op_global_st.sum", "gpu__time_duration.sum"]
+METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__sass_inst_executed_op_global_ld.sum",
+           "smsp__sass_inst_executed_op_global_st.sum", "gpu__time_duration.sum"]
 
 
 def run_case(name, m, n):
@@ -69,7 +69,10 @@ def ncu_case(name, m, n):
     for r in rows[start + 1:]:
         if len(r) <= vi:
             continue
-        val = float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
+        try:
+            val = float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
+        except ValueError:  # "n/a": metric not collected for this kernel
+            continue
         tot[r[ni]] = tot.get(r[ni], 0.0) + val
         kernels[r[ki].split("(")[0]] = 1
     tot["kernels"] = sorted(kernels)
@@ -109,11 +112,12 @@ def main():
         if "error" not in meas:
             rd = meas.get("dram__bytes_read.sum", 0.0)
             row["dram_read_ratio"] = round(rd / exp["dram_read_expected"], 4)
-            ld = meas.get("smsp__sass_thread_inst_executed_op_global_ld.sum")
-            st = meas.get("smsp__sass_thread_inst_executed_op_global_st.sum")
+            ld = meas.get("smsp__sass_inst_executed_op_global_ld.sum")
+            st = meas.get("smsp__sass_inst_executed_op_global_st.sum")
             if ld is not None and CASES[name][4] == "ablation":
-                row["thread_loads_ratio"] = round(ld / exp["thread_loads_total"], 4)
-                row["thread_stores_ratio"] = round(st / exp["thread_stores_total"], 4) if st is not None else None
+                # ncu counts warp instructions; every lane is active (m a multiple of t1 = 128)
+                row["thread_loads_ratio"] = round(32 * ld / exp["thread_loads_total"], 4)
+                row["thread_stores_ratio"] = round(32 * st / exp["thread_stores_total"], 4) if st is not None else None
         res["cases"][name] = row
         print(json.dumps({name: {k_: v_ for k_, v_ in row.items() if k_ != "expected"}}), flush=True)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
