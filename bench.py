@@ -261,6 +261,7 @@ def run_reference_arm(args, wl):
               f"(kernels.py:391-416) restated in numpy (oracle/reference.py), row slabs on {threads} threads "
               f"(the reference itself is single-threaded numpy, so this arm is {threads}x generous to it); the "
               f"rate is per element of A, linear in the columns sampled, so it extrapolates to the full k")
+    pkg = reference_package_rate(m, k, n, prec, c_is_zero)
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / len(times), 3),
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
@@ -268,8 +269,44 @@ def run_reference_arm(args, wl):
             "config": bench_config(wl, args.gpus), "sample": sample,
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": sample},
-            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "reference_package": pkg}
     print(json.dumps(line), flush=True)
+
+
+def reference_package_rate(m, k, n, prec, c_is_zero, budget_s=8.0):
+    """The UNMODIFIED reference (baseline/_ref, tools/install_reference.sh): tsgemm.kernels.run_native
+    on a bounded sample of the workload, single-threaded as it is written — beside the port's
+    all-threads rate, to show the port is the reference's speed per core, not slower."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isfile(os.path.join(ref_dir, "tsgemm", "__init__.py")):
+        return None
+    import numpy as np
+    if ref_dir not in sys.path:
+        sys.path.append(ref_dir)
+    from tsgemm.core import KernelParams, Matrix, Precision, Variant
+    from tsgemm.kernels import run_native
+
+    from oracle.rng import uniform_block
+    P = Precision.DOUBLE if prec == "double" else Precision.SINGLE
+    rows = min(m, 30720 if k > 64 else 1 << 20)
+    cols = min(k, 64)
+    A = uniform_block(range(rows), range(cols), 1, P.dtype)
+    B = uniform_block(range(cols), range(n), 2, P.dtype)
+    mA, mB = Matrix.from_2d(A, P), Matrix.from_2d(B, P)
+    mC = Matrix.zeros(rows, n, P)
+    v = Variant.V3 if k > 64 else Variant.L_OPT2
+    params = KernelParams(t1=128, t2=n, t3=4, tcf=1, variant=v)
+    t_end, reps, t_tot = time.perf_counter() + budget_s, 0, 0.0
+    while reps == 0 or time.perf_counter() < t_end:
+        t0 = time.perf_counter()
+        run_native(v, mA, mB, mC, params)
+        t_tot += time.perf_counter() - t0
+        reps += 1
+    rate = 2.0 * rows * cols * n * reps / t_tot / 1e9
+    return {"value": round(rate, 4), "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"tsgemm.kernels.run_native (baseline/_ref, unmodified) on A[:{rows}, :{cols}] (n={n}, {prec}), "
+                      f"{reps} calls, one thread as written (numpy elementwise ops)"}
 
 
 # ------------------------------------------------------------------------------------------------

@@ -140,6 +140,12 @@ struct SwzOf : std::false_type {};
 template <typename C>
 struct SwzOf<C, std::void_t<decltype(C::kSwz)>> : std::integral_constant<bool, C::kSwz> {};
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ void red_add(double* p, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
@@ -585,6 +591,10 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
   longlong2* meta = reinterpret_cast<longlong2*>(empty + STAGES);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // diagnostic build: per-CTA timeline (globaltimer ns) at dbg[16 + 5*cta + {0 entry, 1 first TMA
+  // issue, 2 first stage landed, 3 producer done, 4 consumers done}]
+  KDIAG(unsigned long long* tl = a.dbg ? a.dbg + 16 + 5 * blockIdx.x : nullptr;
+        if (tl && threadIdx.x == 0) tl[0] = gtimer();)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -634,6 +644,7 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
             const int s = it % STAGES;
             const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
             mbar_wait(&empty[s], ph ^ 1u);
+            KDIAG(if (tl && it == 0) tl[1] = gtimer();)
             meta[s] = make_longlong2(rb | (nst << 32), item);
             mbar_arrive_expect_tx(&full[s], tx);
             if constexpr (SwzOf<Consumer>::value) {
@@ -654,6 +665,7 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
         }
       }
       if (!prep_done) flush_bt();
+      KDIAG(if (tl) tl[3] = gtimer();)
       // end-of-work marker for the consumers
       const int s = it % STAGES;
       mbar_wait(&empty[s], ((uint32_t)(it / STAGES) & 1u) ^ 1u);
@@ -686,6 +698,7 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
     typename Consumer::Frag f0, f1;
     KDIAG(cons.dg = a.diag;)
     mbar_wait(&full[0], 0u);
+    KDIAG(if (tl && threadIdx.x == 32) tl[2] = gtimer();)
     int left;
     {
       const longlong2 md = meta[0];
@@ -753,6 +766,7 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
       s = s1;
     }
     KDIAG(if (a.dbg && threadIdx.x == 32) {
+      tl[4] = gtimer();
       atomicAdd(a.dbg + 0, c_wait);
       atomicAdd(a.dbg + 1, clock64() - t_start);  // "stage" = whole loop time
       atomicAdd(a.dbg + 2, c_fin);
@@ -768,7 +782,8 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
     const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
     KDIAG(const unsigned long long t0c = clock64();)
     mbar_wait(&full[s], ph);
-    KDIAG(const unsigned long long t1c = clock64(); c_wait += t1c - t0c;)
+    KDIAG(const unsigned long long t1c = clock64(); c_wait += t1c - t0c;
+          if (tl && it == 0 && threadIdx.x == 32) tl[2] = gtimer();)
     if (left == 0) {
       const longlong2 md = meta[s];
       if (md.y < 0) {  // end marker (a CTA may get no item at all)
@@ -791,6 +806,7 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
     KDIAG(c_stage += clock64() - t2c; ++n_st;)
   }
   KDIAG(if (a.dbg && threadIdx.x == 32) {
+    tl[4] = gtimer();
     atomicAdd(a.dbg + 0, c_wait);
     atomicAdd(a.dbg + 1, c_stage);
     atomicAdd(a.dbg + 2, c_fin);

@@ -705,9 +705,10 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
 #ifdef TSM2X_TC32_DIAG
   static unsigned long long* dbg = nullptr;
   const bool diag = getenv("TSM2X_TC_DIAG") != nullptr;
+  constexpr int kDbg = 16 + 5 * 1024;  // counters + per-CTA timeline (tsm2r_stream_tma)
   if (diag) {
-    if (!dbg) TSM2X_CUDA(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
-    TSM2X_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), s));
+    if (!dbg) TSM2X_CUDA(cudaMalloc(&dbg, kDbg * sizeof(unsigned long long)));
+    TSM2X_CUDA(cudaMemsetAsync(dbg, 0, kDbg * sizeof(unsigned long long), s));
     a.dbg = dbg;
     a.diag = atoi(getenv("TSM2X_TC_DIAG"));
   }
@@ -735,12 +736,28 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
     TSM2X_TRY((launch_tma_kernel<T, NT, kFma, RPT, CW, SB>(a, tmap, G, s)));
 #ifdef TSM2X_TC32_DIAG
   if (diag) {
-    unsigned long long h[16];
-    TSM2X_CUDA(cudaMemcpyAsync(h, dbg, sizeof h, cudaMemcpyDeviceToHost, s));
+    std::vector<unsigned long long> h(kDbg);
+    TSM2X_CUDA(cudaMemcpyAsync(h.data(), dbg, kDbg * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     TSM2X_CUDA(cudaStreamSynchronize(s));
     const double ns = h[4] ? (double)h[4] : 1.0;
-    fprintf(stderr, "{\"tma_diag\": \"consumer %d\", \"stages\": %llu, \"wait_full\": %.0f, \"stage\": %.0f, \"finish\": %.0f}\n",
-            kind, h[4], h[0] / ns, h[1] / ns, h[2] / ns);
+    // per-CTA timeline relative to the first CTA's entry: median / max of each event (us)
+    unsigned long long t00 = ~0ull;
+    for (int64_t c = 0; c < G; ++c) t00 = std::min(t00, h[16 + 5 * c]);
+    double med[5], mx[5];
+    for (int e = 0; e < 5; ++e) {
+      std::vector<double> v;
+      for (int64_t c = 0; c < G; ++c)
+        if (h[16 + 5 * c + e]) v.push_back((h[16 + 5 * c + e] - t00) * 1e-3);
+      std::sort(v.begin(), v.end());
+      med[e] = v.empty() ? -1 : v[v.size() / 2];
+      mx[e] = v.empty() ? -1 : v.back();
+    }
+    fprintf(stderr,
+            "{\"tma_diag\": \"consumer %d\", \"stages\": %llu, \"wait_full\": %.0f, \"stage\": %.0f, \"finish\": %.0f, "
+            "\"timeline_us\": {\"entry\": [%.2f, %.2f], \"first_tma\": [%.2f, %.2f], \"first_stage\": [%.2f, %.2f], "
+            "\"producer_done\": [%.2f, %.2f], \"consumers_done\": [%.2f, %.2f]}, \"ctas\": %lld}\n",
+            kind, h[4], h[0] / ns, h[1] / ns, h[2] / ns, med[0], mx[0], med[1], mx[1], med[2], mx[2], med[3], mx[3],
+            med[4], mx[4], (long long)G);
   }
 #endif
   if (timed) {
