@@ -219,8 +219,12 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
                    &full[pend_s[i]]);
         npend = 0;
       };
+      bool first_grab = true;  // static first grab, as tsm2r_stream_tma
       for (;;) {
-        const int64_t first = (int64_t)atomicAdd(a.queue, (unsigned long long)a.it.batch);
+        const int64_t first =
+            first_grab ? (int64_t)blockIdx.x * a.it.batch
+                       : (int64_t)gridDim.x * a.it.batch + (int64_t)atomicAdd(a.queue, (unsigned long long)a.it.batch);
+        first_grab = false;
         if (first >= a.it.total) break;
         const int64_t last = min64(first + a.it.batch, a.it.total);
         for (int64_t item = first; item < last; ++item) {

@@ -1,8 +1,7 @@
-python tools/small_probe.py 4096 8 > gpurun_out/small_probe_r02b.jsonl 2>&1
-TSM2X_CONSUMER=null python tools/small_probe.py 4096 8 >> gpurun_out/small_probe_r02b.jsonl 2>&1
-TSM2X_STAGE_KB=32 python tools/small_probe.py 4096 8 >> gpurun_out/small_probe_r02b.jsonl 2>&1
-TSM2X_MID_MB=0 python tools/small_probe.py 4096 8 >> gpurun_out/small_probe_r02b.jsonl 2>&1
-TSM2X_SWZ=0 python tools/small_probe.py 4096 8 >> gpurun_out/small_probe_r02b.jsonl 2>&1
-python tools/small_probe.py 1024 8 >> gpurun_out/small_probe_r02b.jsonl 2>&1
-cat gpurun_out/small_probe_r02b.jsonl
-timeout 300 python bench.py --workload tsm2r_fp64_n8_4096 --steps 50 --warmup 5 > gpurun_out/bench_r02c_4096.jsonl 2>gpurun_out/bench_r02c.err; cut -c1-1800 gpurun_out/bench_r02c_4096.jsonl; grep -i error gpurun_out/bench_r02c.err | tail -3
+python tools/small_probe.py 4096 8 2>&1 | grep read_flush
+python tools/small_probe.py 2048 8 2>&1 | grep read_flush
+export TSM2X_LIB_PATH_EXPERIMENT=paper_2002_03258_b200/libtsm2x_diag.so
+TSM2X_TC_DIAG=0 python tools/timeline_probe.py 4096 8 2>&1 | grep -E "tma_diag" | tail -2
+unset TSM2X_LIB_PATH_EXPERIMENT
+timeout 600 python -m pytest tests/test_parity_gpu.py -q -m gpu -x 2>&1 | tail -2
+python bench.py --steps 100 --warmup 10 --e2e-steps 0 --no-cpu-baseline | cut -c1-400

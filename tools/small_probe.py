@@ -40,7 +40,8 @@ def graph_us(fn, pre, reps=40):
         ts.append((e0, e1))
     torch.cuda.synchronize()
     us = sorted(a.elapsed_time(b) * 1e3 for a, b in ts)
-    return us[len(us) // 2]
+    mid = us[len(us) // 4: len(us) - len(us) // 4]  # event timestamps are ~2 us granular here: average
+    return sum(mid) / len(mid)                      # the middle half instead of taking the median
 
 
 def main():
