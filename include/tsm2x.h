@@ -116,6 +116,14 @@ int tsm2x_run_host_multi(int variant, int precision, int64_t m, int64_t k, int64
                          const void* C_in, void* C_out, int64_t ldc,
                          const tsm2x_params* params, uint32_t flags, int ndev, const int* devices);
 
+/* Frees the library's cached device memory on `device` (-1 = every device): the per-(device,
+ * stream) workspaces (Bt, fp64 accumulators, queue counters; kept across calls and grown on
+ * demand) and the host path's staging buffers, pinned buffers, events and streams. Synchronises
+ * the device first. Call it when a long-lived process is done with a set of streams (workspaces
+ * are keyed by stream, so a process that keeps creating streams would otherwise keep their
+ * workspaces); later calls re-allocate what they need. Not a reference interface. */
+int tsm2x_release_cached(int device);
+
 /* Synthetic-input utility (not a reference interface): fills the rows x cols column-major
  * block at ptr (leading dimension ld) with the counter-based uniform [0, 1) generator
  *   x = splitmix64(seed * 0x9E3779B97F4A7C15 + ((col_offset + j) << 32 | (row_offset + i)))

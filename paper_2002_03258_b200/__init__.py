@@ -12,7 +12,15 @@ from .core import (  # noqa: F401
     Variant,
     validate_problem,
 )
-from .kernels import colmajor_empty, fill_uniform, gemm, run_native, run_native_multi, simulate  # noqa: F401
+from .kernels import (  # noqa: F401
+    colmajor_empty,
+    fill_uniform,
+    gemm,
+    release_cached_memory,
+    run_native,
+    run_native_multi,
+    simulate,
+)
 
 __all__ = [
     "KernelParams",
@@ -23,6 +31,7 @@ __all__ = [
     "colmajor_empty",
     "fill_uniform",
     "gemm",
+    "release_cached_memory",
     "run_native",
     "run_native_multi",
     "simulate",

@@ -89,10 +89,11 @@ def load() -> ctypes.CDLL:
         lib.tsm2x_set_tuning.argtypes = [ctypes.POINTER(Tuning)]
         lib.tsm2x_get_tuning.argtypes = [ctypes.POINTER(Tuning)]
         lib.tsm2x_plan_for.argtypes = [i32, i64, i64, i64, i64, i32, u32, i32, ctypes.POINTER(Plan)]
+        lib.tsm2x_release_cached.argtypes = [i32]
         for name in ("tsm2x_validate", "tsm2x_run", "tsm2x_run_ex", "tsm2x_run_host", "tsm2x_run_host_multi",
                      "tsm2x_fill_uniform",
                      "tsm2x_version", "tsm2x_set_kernel_events", "tsm2x_set_tuning", "tsm2x_get_tuning",
-                     "tsm2x_plan_for"):
+                     "tsm2x_plan_for", "tsm2x_release_cached"):
             getattr(lib, name).restype = ctypes.c_int
         lib.tsm2x_last_error.restype = ctypes.c_char_p
         lib.tsm2x_build_target.restype = ctypes.c_char_p

@@ -1328,6 +1328,25 @@ struct HostCtx {
     return TSM2X_OK;
   }
   void begin() { ev_next = 0; }
+  // frees every cached buffer, event and stream (tsm2x_release_cached); the context re-initialises
+  // on its next use
+  void release() {
+    drain();
+    for (auto& e : dbufs)
+      if (e.second.first) cudaFree(e.second.first);
+    for (auto& e : hbufs)
+      if (e.second.first) cudaFreeHost(e.second.first);
+    dbufs.clear();
+    hbufs.clear();
+    for (auto e : events) cudaEventDestroy(e);
+    events.clear();
+    ev_next = 0;
+    for (cudaStream_t* st : {&h2d, &comp, &d2h})
+      if (*st) {
+        cudaStreamDestroy(*st);
+        *st = nullptr;
+      }
+  }
   void drain() {
     cudaStreamSynchronize(h2d);
     cudaStreamSynchronize(comp);
@@ -1754,6 +1773,56 @@ int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, 
   out->consumer = 1 + pick_consumer_rt(eb, nt, it.nch() > 1, tu);
   if (out->consumer == 1 + kTc) out->consumer = 1 + (nt >= 2 ? kFfma2 : kFma);  // tc path not taken
   out->deterministic = (it.nch() == 1 || tu.combine == 1 || (tu.combine == 0 && determ)) ? 1 : 0;
+  return TSM2X_OK;
+}
+
+int tsm2x_release_cached(int device) {
+  // per-(device, stream) workspaces: every stream that ever called the library on `device` (-1 =
+  // all devices) — synchronised, then freed; the next call on a stream allocates afresh
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (auto it = g_ws.begin(); it != g_ws.end();) {
+      if (device >= 0 && it->first.first != device) {
+        ++it;
+        continue;
+      }
+      {
+        Workspace* w = it->second.get();
+        std::lock_guard<std::mutex> wl(w->mu);  // released before the workspace is destroyed below
+        TSM2X_CUDA(cudaSetDevice(it->first.first));
+        TSM2X_CUDA(cudaDeviceSynchronize());  // the stream itself may already be destroyed
+        // stream-ordered allocations (ws_reserve): freed on the legacy stream after the device sync
+        if (w->buf) TSM2X_CUDA(cudaFreeAsync(w->buf, 0));
+        if (w->counters) TSM2X_CUDA(cudaFreeAsync(w->counters, 0));
+        w->buf = nullptr;
+        w->counters = nullptr;
+        w->cap = w->ccap = 0;
+        w->flag = nullptr;
+      }
+      it = g_ws.erase(it);
+    }
+  }
+  // return the freed blocks of the default memory pools to the driver
+  {
+    int ndev = 0;
+    TSM2X_CUDA(cudaGetDeviceCount(&ndev));
+    for (int d = 0; d < ndev; ++d) {
+      if (device >= 0 && d != device) continue;
+      cudaMemPool_t pool;
+      TSM2X_CUDA(cudaSetDevice(d));
+      TSM2X_CUDA(cudaDeviceSynchronize());
+      TSM2X_CUDA(cudaDeviceGetDefaultMemPool(&pool, d));
+      TSM2X_CUDA(cudaMemPoolTrimTo(pool, 0));
+    }
+  }
+  // host-path contexts: device / pinned staging buffers, events, streams
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  for (auto& e : g_host) {
+    if (device >= 0 && e.first != device) continue;
+    std::lock_guard<std::mutex> hl(e.second->mu);
+    TSM2X_CUDA(cudaSetDevice(e.first));
+    e.second->release();
+  }
   return TSM2X_OK;
 }
 

@@ -186,3 +186,10 @@ def fill_uniform(T, seed: int, row_offset: int = 0, col_offset: int = 0, stream=
                                             seed & 0xFFFFFFFFFFFFFFFF, ctypes.c_void_p(stream.cuda_stream))
     _lib.check(rc)
     return T
+
+
+def release_cached_memory(device: int = -1) -> None:
+    """Frees the library's cached device / pinned memory (per-stream workspaces, host-path staging)
+    on ``device`` (-1: all devices) after synchronising it (``tsm2x_release_cached``). For
+    long-lived processes that create many streams; later calls re-allocate what they need."""
+    _lib.check(_lib.load().tsm2x_release_cached(int(device)))

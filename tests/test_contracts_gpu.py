@@ -150,3 +150,33 @@ def test_bench_config1_flushed():
     d = _json_line(out.stdout)
     assert "flushed" in d["config"]["l2"] and d["value"] > 1000
     assert d["e2e"]["drop_in"]["value"] > 0
+
+
+def test_release_cached_memory_frees_stream_workspaces():
+    """Workspaces are per (device, stream) and kept across calls; release_cached_memory frees them
+    (a process creating many streams otherwise keeps every stream's workspace)."""
+    import torch
+    tsm = _tsm()
+    m, k, n = 65536, 4096, 16  # fp32 split row blocks: Bt + an fp64 accumulator per stream
+    A = tsm.colmajor_empty(m, k, torch.float32, "cuda")
+    tsm.fill_uniform(A, seed=1)
+    B = tsm.colmajor_empty(k, n, torch.float32, "cuda")
+    tsm.fill_uniform(B, seed=2)
+    C = tsm.colmajor_empty(m, n, torch.float32, "cuda")
+    tsm.release_cached_memory()
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    streams = [torch.cuda.Stream() for _ in range(12)]
+    for s in streams:
+        with torch.cuda.stream(s):
+            tsm.gemm(A, B, C, c_is_zero=True)
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 >= 12 * (m * n * 8)  # every stream kept at least its accumulator
+    tsm.release_cached_memory()
+    free2 = torch.cuda.mem_get_info()[0]
+    assert free2 >= free0 - (64 << 20)
+    tsm.gemm(A, B, C, c_is_zero=True)  # the library re-allocates on demand
+    torch.cuda.synchronize()
+    ref = (A.double() @ B.double())
+    assert rel_frobenius(C.double().cpu().numpy(), ref.cpu().numpy()) <= 1e-5

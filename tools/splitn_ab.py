@@ -36,10 +36,20 @@ def per_call_ms(fn, calls=30, blocks=7):
     return statistics.median(out)
 
 
+def _shapes_from_argv():
+    """Optional shapes on the command line: m,k,n,{f64|f32} ..."""
+    out = []
+    for a in sys.argv[1:]:
+        m, k, n, d = a.split(",")
+        out.append((int(m), int(k), int(n), torch.float64 if d == "f64" else torch.float32))
+    return out or SHAPES
+
+
 def main():
+    shapes = _shapes_from_argv()
     print(json.dumps({"what": "TSM2L split-n warp-shuffle A/B (tools/splitn_ab.py); sustained per-call ms, "
                       "C = A*B under the zero-C contract (L_OPT2)"}))
-    for m, k, n, dt in SHAPES:
+    for m, k, n, dt in shapes:
         A = tsm.colmajor_empty(m, k, dt, "cuda")
         tsm.fill_uniform(A, seed=1)
         B = tsm.colmajor_empty(k, n, dt, "cuda")
