@@ -25,6 +25,7 @@ EXPORTS = (
     "tsm2x_run_host",
     "tsm2x_run_host_multi",
     "tsm2x_fill_uniform",
+    "tsm2x_release_cached",
     "tsm2x_last_error",
     "tsm2x_version",
     "tsm2x_build_target",
