@@ -1245,11 +1245,49 @@ static bool is_pinned(const void* p) {
   return at.type == cudaMemoryTypeHost;
 }
 
+// host threads for the pageable staging copies and the zero-C scan
+static unsigned host_threads(size_t bytes) {
+  if (bytes < (8u << 20)) return 1;
+  return std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+}
+
+// reference kernels.py:366-368 (_require_zero_c): L_OPT2 requires an all-zero C — a parallel scan
+// of the host copy with early exit, before any device work (so a CPU-only caller gets the
+// ValueError too)
+template <typename T>
+static bool host_all_zero(const T* C, int64_t m, int64_t n, int64_t ldc) {
+  const unsigned nt = host_threads((size_t)m * n * sizeof(T));
+  std::atomic<bool> nonzero{false};
+  auto scan = [&](unsigned t) {
+    const int64_t j0 = n * t / nt, j1 = n * (t + 1) / nt;
+    if (n >= nt || nt == 1) {
+      for (int64_t j = j0; j < j1 && !nonzero.load(std::memory_order_relaxed); ++j)
+        for (int64_t i = 0; i < m; ++i)
+          if (C[i + j * ldc] != T(0)) {
+            nonzero = true;
+            return;
+          }
+    } else {  // few columns: split the rows instead
+      const int64_t i0 = m * t / nt, i1 = m * (t + 1) / nt;
+      for (int64_t j = 0; j < n && !nonzero.load(std::memory_order_relaxed); ++j)
+        for (int64_t i = i0; i < i1; ++i)
+          if (C[i + j * ldc] != T(0)) {
+            nonzero = true;
+            return;
+          }
+    }
+  };
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < nt; ++t) th.emplace_back(scan, t);
+  scan(0);
+  for (auto& x : th) x.join();
+  return !nonzero.load();
+}
+
 // parallel memcpy (pageable -> pinned staging); 2-D with pitches
 static void par_copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height) {
   const size_t total = width * height;
-  unsigned nt = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
-  if (total < (8u << 20)) nt = 1;
+  const unsigned nt = host_threads(total);
   auto work = [&](unsigned t) {
     if (width == dpitch && width == spitch) {
       size_t lo = total * t / nt, hi = total * (t + 1) / nt;
@@ -1406,13 +1444,7 @@ static int run_host_t(int variant, int64_t m, int64_t k, int64_t n, const T* A, 
   TSM2X_TRY(device_info(device, &di));
   if (lda < m || ldb < k || ldc < m) return fail(TSM2X_EINVAL, "leading dimensions too small");
   bool c_is_zero = (flags & TSM2X_FLAG_C_IS_ZERO) != 0;
-  if (variant == TSM2X_L_OPT2 && !c_is_zero) {
-    // reference kernels.py:366-368: L_OPT2 requires an all-zero C (checked on the host copy)
-    for (int64_t j = 0; j < n; ++j)
-      for (int64_t i = 0; i < m; ++i)
-        if (Cin[i + j * ldc] != T(0)) return fail(TSM2X_EINVAL, "L_OPT2 stores partial sums to C and requires a zeroed C");
-    c_is_zero = true;
-  }
+  if (variant == TSM2X_L_OPT2) c_is_zero = true;  // tsm2x_run_host checked C == 0 on the host
   HostCtx* hc = host_ctx(device);
   std::lock_guard<std::mutex> lk(hc->mu);
   TSM2X_TRY(hc->init(device));
@@ -1598,6 +1630,13 @@ int tsm2x_run_host(int variant, int precision, int64_t m, int64_t k, int64_t n, 
                    const tsm2x_params* params, uint32_t flags, int device) {
   TSM2X_TRY(validate(variant, precision, m, k, n, params));
   if (!A || !B || !C_out || (!C_in && !(flags & TSM2X_FLAG_C_IS_ZERO))) return fail(TSM2X_EINVAL, "null host pointer");
+  if (ldc < m) return fail(TSM2X_EINVAL, "leading dimensions too small");
+  if (variant == TSM2X_L_OPT2 && !(flags & TSM2X_FLAG_C_IS_ZERO)) {
+    const bool zero = precision == TSM2X_DOUBLE ? host_all_zero((const double*)C_in, m, n, ldc)
+                                                : host_all_zero((const float*)C_in, m, n, ldc);
+    if (!zero) return fail(TSM2X_EINVAL, "L_OPT2 stores partial sums to C and requires a zeroed C");
+    flags |= TSM2X_FLAG_C_IS_ZERO;
+  }
   if (precision == TSM2X_DOUBLE)
     return run_host_t<double>(variant, m, k, n, (const double*)A, lda, (const double*)B, ldb, (const double*)C_in,
                               (double*)C_out, ldc, params, flags, device);

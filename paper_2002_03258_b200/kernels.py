@@ -45,11 +45,10 @@ def _host_call(variant, A, B, C, params, deterministic):
     prec = Precision.coerce(A.precision)
     dtype = prec.dtype
     a, b, c = _flat(A, dtype), _flat(B, dtype), _flat(C, dtype)
+    # L_OPT2's zero-C rule (reference kernels.py:366-368) is checked by tsm2x_run_host on the host
+    # copy — a parallel scan with early exit, before any device work — and raises the same
+    # ValueError through _lib.check
     flags = _lib.FLAG_DETERMINISTIC if deterministic else 0
-    if variant is Variant.L_OPT2:
-        if np.any(c != 0):
-            raise ValueError("L_OPT2 stores partial sums to C and requires a zeroed C")
-        flags |= _lib.FLAG_C_IS_ZERO
     return variant, m, k, n, prec, a, b, c, flags
 
 
