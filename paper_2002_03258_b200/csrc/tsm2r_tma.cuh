@@ -113,6 +113,9 @@ struct DynArgs {
   unsigned* tickets;  // [num_rb] next chunk allowed to update the row block; zero between launches
   Items it;
   unsigned long long* queue;  // [0] next item, [1] low 32 bits: producers finished
+  const T* B = nullptr;  // inline_b: the pass's B (k x w, column-major, ldb) — no prep kernel
+  int64_t ldb = 0;
+  int inline_b = 0;      // 1: the producer warp builds each stage's Bt rows from B itself
   int l2pol = 0;                      // L2 policy of the A stream (policy_for; TSM2X_L2POL)
   int diag = 0;                       // tsm2r_stream_tc32 diagnostics (TSM2X_TC_DIAG): skip bits
   unsigned long long* dbg = nullptr;  // tsm2r_stream_tc32 diagnostics: cycle counters (or null)
@@ -139,6 +142,56 @@ template <typename C, typename = void>
 struct SwzOf : std::false_type {};
 template <typename C>
 struct SwzOf<C, std::void_t<decltype(C::kSwz)>> : std::integral_constant<bool, C::kSwz> {};
+
+// Element i of Bt (the per-pass copy of B the stage ring reads): row-major kpad x NT (FMA /
+// FFMA2 consumers) or, FRAG, DMMA fragment order — for each group of 4 B rows (kg) and N tile
+// (nt) the 32 values in lane order, lane (g = lane/4, t = lane%4) holding B[row][8nt + g] with
+// row = 4kg + t, or on the swizzled A layout row = 8(kg/2) + 2t + kg%2 (k-step kg takes columns
+// {0,2,4,6} / {1,3,5,7} of an 8-column group). Zero outside k x w. Used by prep_dyn and by the
+// stream kernel's inline-B producer.
+template <typename T, int NT, bool FRAG>
+__device__ __forceinline__ T bt_elem(const T* __restrict__ B, int64_t ldb, int64_t k, int w, bool swz, int64_t i) {
+  if constexpr (FRAG) {
+    const int lane = (int)(i % 32);
+    const int64_t tile = i / 32;
+    const int nt = (int)(tile % (NT / 8));
+    const int64_t kg = tile / (NT / 8);
+    const int64_t row = swz ? 8 * (kg >> 1) + 2 * (lane & 3) + (kg & 1) : 4 * kg + (lane & 3);
+    const int col = 8 * nt + (lane >> 2);
+    return (row < k && col < w) ? __ldg(B + row + col * ldb) : T(0);
+  } else {
+    const int64_t c = i / NT;
+    const int j = (int)(i - c * NT);
+    return (j < w && c < k) ? __ldg(B + c + j * ldb) : T(0);
+  }
+}
+
+// Inverse of bt_elem: the Bt index of B[row][col] (row < kpad, col < NT).
+template <int NT, bool FRAG>
+__device__ __forceinline__ int64_t bt_index(int64_t row, int col, bool swz) {
+  if constexpr (FRAG) {
+    const int nt = col >> 3, g = col & 7;
+    int64_t kg;
+    int t;
+    if (swz) {
+      const int within = (int)(row & 7);
+      kg = 2 * (row >> 3) + (within & 1);
+      t = within >> 1;
+    } else {
+      kg = row >> 2;
+      t = (int)(row & 3);
+    }
+    return (kg * (NT / 8) + nt) * 32 + g * 4 + t;
+  } else {
+    return row * NT + col;
+  }
+}
+
+// Consumers that read B in DMMA fragment order (every DmmaConsumer, which declares kSwz).
+template <typename C, typename = void>
+struct FragOf : std::false_type {};
+template <typename C>
+struct FragOf<C, std::void_t<decltype(C::kSwz)>> : std::true_type {};
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -610,6 +663,122 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
   // before the first Bt copy is due (the stage barriers expect both); the consumers wait at once
   // (they write C / the accumulator, which prep may have zeroed).
 
+  if (warp == 0 && a.inline_b) {
+    // ---------------- producer, inline B (one launch per call, no prep kernel).
+    // The whole warp runs the loop. Lane 0 takes items and issues the A tensor loads exactly as
+    // the prep-fed producer does; the 32 lanes gather each stage's KC rows of B (in the
+    // consumer's Bt order, bt_elem) into registers and store them next to the A tile one
+    // iteration later — after the NEXT stage's tensor load has been issued — so the gather's
+    // L2 latency never sits between a free slot and its TMA issue. A stage's barrier expects the
+    // TMA bytes (expect_tx, no arrival) before its loads are issued and completes on lane 0's
+    // arrival after the B stores (__syncwarp orders the other lanes' stores before it).
+    // Launched without programmatic serialization, so A and B are complete when the kernel starts.
+    const uint64_t pol = policy_for(a.l2pol);
+    constexpr int PER = (Cfg::B_ELEMS + 31) / 32;
+    constexpr bool kFrag = FragOf<Consumer>::value;
+    constexpr bool kSwzB = SwzOf<Consumer>::value;
+    // stage cursor: current item range [item, last), the item's row block and column range
+    int64_t item = 0, last = 0, rb = 0, col = 0, col1 = 0, nst = 0;
+    int nbox = 0;
+    auto open_item = [&]() {
+      int64_t col0;
+      a.it.decode(item, a.k, &rb, &col0, &col1);
+      col = col0;
+      nst = (col1 - col0 + KC - 1) / KC;
+      nbox = (int)min64(Cfg::NBOX, (a.m - rb * R + Cfg::BOX - 1) / Cfg::BOX);
+    };
+    // the first grab of every CTA is static (item block blockIdx.x), later ones from the queue
+    auto grab = [&](bool first_grab) -> bool {
+      int64_t first;
+      if (first_grab) {
+        first = (int64_t)blockIdx.x * a.it.batch;
+      } else {
+        unsigned long long q = 0;
+        if (lane == 0) q = atomicAdd(a.queue, (unsigned long long)a.it.batch);
+        q = __shfl_sync(0xffffffffu, q, 0);
+        first = (int64_t)gridDim.x * a.it.batch + (int64_t)q;
+      }
+      if (first >= a.it.total) return false;
+      item = first;
+      last = min64(first + a.it.batch, a.it.total);
+      open_item();
+      return true;
+    };
+    bool have = grab(true);
+    int it = 0;
+    T v[PER];
+    int prev_s = -1;  // slot whose B rows are in v, still to be stored and published
+    while (have) {
+      const int s = it % STAGES;
+      const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+      if (lane == 0) {  // one lane polls (32 polling lanes would take smem cycles from the consumers)
+        mbar_wait(&empty[s], ph ^ 1u);
+        KDIAG(if (tl && it == 0) tl[1] = gtimer();)
+        meta[s] = make_longlong2(rb | (nst << 32), item);
+        mbar_expect_tx(&full[s], kSwzB ? (uint32_t)Cfg::A_BYTES : (uint32_t)(nbox * Cfg::BOX * KC * (int)sizeof(T)));
+        if constexpr (kSwzB) {
+          tma_load_3d(sA + (size_t)s * Cfg::A_ELEMS, &tmA, 0, (int)col, (int)(rb * R / 16), &full[s], pol);
+        } else {
+          for (int b = 0; b < nbox; ++b)
+            tma_load_2d(sA + (size_t)s * Cfg::A_ELEMS + b * (Cfg::BOX * KC), &tmA, (int)(rb * R + b * Cfg::BOX),
+                        (int)col, &full[s], pol);
+        }
+      }
+      if (prev_s >= 0) {  // the previous stage's B rows (gathered one iteration ago)
+        T* dst = sB + (size_t)prev_s * (Cfg::B_BYTES_PAD / sizeof(T));
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+          const int idx = lane + 32 * j;
+          if (idx < Cfg::B_ELEMS) dst[bt_index<NT, kFrag>(idx % KC, idx / KC, kSwzB)] = v[j];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[prev_s]);
+      }
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int idx = lane + 32 * j;
+        // source order (KC consecutive rows of one B column per group of KC lanes: whole 128-B
+        // lines per warp load); the stores scatter into the consumer's Bt order (bt_index)
+        const int r = idx % KC, c = idx / KC;
+        v[j] = (idx < Cfg::B_ELEMS && col + r < a.k && c < a.w) ? __ldg(a.B + (col + r) + (int64_t)c * a.ldb) : T(0);
+      }
+      prev_s = s;
+      ++it;
+      // advance the cursor: next stage of this item, next item of the batch, or a new grab
+      col += KC;
+      if (col >= col1) {
+        if (++item < last)
+          open_item();
+        else
+          have = grab(false);
+      }
+    }
+    if (prev_s >= 0) {
+      T* dst = sB + (size_t)prev_s * (Cfg::B_BYTES_PAD / sizeof(T));
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int idx = lane + 32 * j;
+        if (idx < Cfg::B_ELEMS) dst[bt_index<NT, kFrag>(idx % KC, idx / KC, kSwzB)] = v[j];
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (prev_s >= 0) mbar_arrive(&full[prev_s]);
+      KDIAG(if (tl) tl[3] = gtimer();)
+      const int s = it % STAGES;
+      mbar_wait(&empty[s], ((uint32_t)(it / STAGES) & 1u) ^ 1u);
+      meta[s] = make_longlong2(-1, -1);
+      mbar_arrive(&full[s]);
+      __threadfence();
+      const unsigned prev = atomicAdd(reinterpret_cast<unsigned*>(a.queue + 1), 1u);
+      if (prev == gridDim.x - 1) {
+        a.queue[0] = 0ull;
+        a.queue[1] = 0ull;
+        __threadfence();
+      }
+    }
+    return;
+  }
   if (warp == 0) {
     // ---------------- producer
     if (lane == 0) {
@@ -854,19 +1023,7 @@ __global__ void prep_dyn(const T* __restrict__ B, int64_t ldb, int64_t k, int64_
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nb + nz; i += stride) {
     if (i < nb) {
-      if constexpr (FRAG) {
-        const int lane = (int)(i % 32);
-        const int64_t tile = i / 32;
-        const int nt = (int)(tile % (NT / 8));
-        const int64_t kg = tile / (NT / 8);
-        const int64_t row = swz ? 8 * (kg >> 1) + 2 * (lane & 3) + (kg & 1) : 4 * kg + (lane & 3);
-        const int col = 8 * nt + (lane >> 2);
-        Bt[i] = (row < k && col < w) ? B[row + col * ldb] : T(0);
-      } else {
-        const int64_t c = i / NT;
-        const int j = (int)(i - c * NT);
-        Bt[i] = (j < w && c < k) ? B[c + j * ldb] : T(0);
-      }
+      Bt[i] = bt_elem<T, NT, FRAG>(B, ldb, k, w, swz != 0, i);
     } else {
       const int64_t z = i - nb, col = z / zrows, row = z - col * zrows;
       zp[row + col * zld] = Z(0);

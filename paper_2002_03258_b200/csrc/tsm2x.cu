@@ -610,6 +610,8 @@ struct ConsumerFor<float, NT, kFfma2, RPT, CW, SB> {
 
 template <typename T, int NT, int KIND, int RPT, int CW, int SB = 32768>
 static int launch_tma_kernel(const DynArgs<T>& a_in, const CUtensorMap& tmap_in, int64_t G, cudaStream_t s) {
+  // inline B: the kernel is the call's first launch, so it must not start before the previous
+  // work on the stream has finished (no programmatic serialization)
   using Cons = typename ConsumerFor<T, NT, KIND, RPT, CW, SB>::type;
   using Cfg = typename Cons::Cfg;
   static_assert(Cfg::R == TmaCfg<T, NT, RPT, CW, SB>::R && Cfg::KC == TmaCfg<T, NT, RPT, CW, SB>::KC,
@@ -628,7 +630,7 @@ static int launch_tma_kernel(const DynArgs<T>& a_in, const CUtensorMap& tmap_in,
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = a.inline_b ? 0 : 1;
   TSM2X_CUDA(cudaLaunchKernelEx(&cfg, kern, a, tmap));
   return check_launch("tsm2r_stream_tma");
 }
@@ -674,18 +676,36 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   a.Bt = reinterpret_cast<T*>(ws->buf);
   a.acc = acc_bytes ? reinterpret_cast<double*>(static_cast<char*>(ws->buf) + bt_bytes) : nullptr;
   a.queue = reinterpret_cast<unsigned long long*>(ws->counters);  // zero between launches
-  {
-    // one prep launch: Bt, plus the zeroed accumulation target of split row blocks
-    double* zp = nullptr;
-    int64_t zld = 0, zrows = 0;
-    if (atomic_split && sizeof(T) == 4) {
-      zp = a.acc;
-      zld = zrows = a.ldacc;
-    } else if (atomic_split && c_is_zero) {
-      zp = reinterpret_cast<double*>(C);
-      zld = ldc;
-      zrows = m;
-    }
+  // the zeroed accumulation target of split row blocks (C itself for fp64 under the zero-C
+  // contract, the fp64 accumulator for fp32), if any
+  double* zp = nullptr;
+  int64_t zld = 0, zrows = 0;
+  if (atomic_split && sizeof(T) == 4) {
+    zp = a.acc;
+    zld = zrows = a.ldacc;
+  } else if (atomic_split && c_is_zero) {
+    zp = reinterpret_cast<double*>(C);
+    zld = ldc;
+    zrows = m;
+  }
+  // inline B (no prep kernel, the producer warp gathers each stage's Bt rows from B itself):
+  // taken when there is nothing to zero and either the call is small (A <= 256 MB: one launch
+  // per call instead of two, BASELINE configs[0] 30.3 -> 28.6 us) or the pass is the fp64 DMMA
+  // 8-column tile (n = 3..8: -1.9 to -2.2 % sustained at 30720^2). Wider / FMA passes keep prep:
+  // the per-stage gather costs shared-memory cycles at n = 16 (+3.5 %) and L2 latency in the
+  // producer loop on the short 32 KB stages of n = 2 (+9 %) (profiles/inline_b_r02.json).
+  // TSM2X_INLINE_B = 0 never, 1 always, unset = this rule.
+  static const int inline_env = env_int("TSM2X_INLINE_B", -1);
+  const bool frag8 = sizeof(T) == 8 && NT == 8 && (kind == kDmma || kind == kDmmaP);
+  const bool want_inline =
+      inline_env == 1 || (inline_env < 0 && ((double)m * (double)k * (double)eb <= 256.0 * 1048576.0 || frag8));
+  if (!zp && want_inline) {
+    a.inline_b = 1;
+    a.B = B;
+    a.ldb = ldb;
+  }
+  if (!a.inline_b) {
+    // one prep launch: Bt, plus the zeroed accumulation target
     const int64_t tot = kpad * NT + (zp ? zrows * w : 0);
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, (int64_t)di.sms * 16));
     if constexpr (sizeof(T) == 8 && (NT == 8 || NT == 16)) {
