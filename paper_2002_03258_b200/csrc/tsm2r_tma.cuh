@@ -247,29 +247,49 @@ __device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int
   const int64_t c = nch == 1 ? 0 : a.it.chunk(item);
   if (nch == 1 || a.ordered) {
     if (nch > 1) ticket_wait(a.tickets + rb, (unsigned)c, ct == 0);
-    // all loads of C first (one round trip, not NT*RPT dependent ones), then the stores; the
-    // first chunk starts from C's input (or from zero under the zero-C contract)
+    // the first chunk starts from C's input (or from zero under the zero-C contract)
     const bool read_c = c > 0 || !a.c_is_zero;
-    T old[RPT][NT];
+    if (!read_c) {
+      // zero-C single-chunk row blocks (TSM2L): plain streaming stores, C never read
 #pragma unroll
-    for (int j = 0; j < NT; ++j)
+      for (int j = 0; j < NT; ++j) {
+        if (j >= a.w) continue;
+        T* cj = a.C + j * a.ldc;
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        const int64_t row = row_base + r * CT;
-        old[r][j] = (read_c && j < a.w && row < a.m) ? __ldcg(a.C + j * a.ldc + row) : T(0);
+        for (int r = 0; r < RPT; ++r) {
+          const int64_t row = row_base + r * CT;
+          if (row < a.m) __stcs(cj + row, acc[r][j]);
+        }
       }
+    } else {
+      // loads of a group of columns first (one round trip per group, not per element), then
+      // their stores; groups of 4 columns bound the live registers (a whole 16-column tile of
+      // loaded C spilled at RPT = 4)
+      constexpr int G = NT < 4 ? NT : 4;
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      if (j >= a.w) continue;
-      T* cj = a.C + j * a.ldc;
+      for (int j0 = 0; j0 < NT; j0 += G) {
+        T old[RPT][G];
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        const int64_t row = row_base + r * CT;
-        if (row < a.m) {
-          if (nch == 1)
-            __stcs(cj + row, old[r][j] + acc[r][j]);
-          else
-            __stcg(cj + row, old[r][j] + acc[r][j]);
+        for (int jj = 0; jj < G; ++jj)
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const int64_t row = row_base + r * CT;
+            old[r][jj] = (j0 + jj < a.w && row < a.m) ? __ldcg(a.C + (j0 + jj) * a.ldc + row) : T(0);
+          }
+#pragma unroll
+        for (int jj = 0; jj < G; ++jj) {
+          if (j0 + jj >= a.w) continue;
+          T* cj = a.C + (j0 + jj) * a.ldc;
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const int64_t row = row_base + r * CT;
+            if (row < a.m) {
+              if (nch == 1)
+                __stcs(cj + row, old[r][jj] + acc[r][j0 + jj]);
+              else
+                __stcg(cj + row, old[r][jj] + acc[r][j0 + jj]);
+            }
+          }
         }
       }
     }

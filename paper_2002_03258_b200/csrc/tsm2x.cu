@@ -452,12 +452,19 @@ static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
   // (TSM2R) use the k-step software-pipelined loop (-4.8 % n=16, -1.1 % n=8 sustained);
   // single-chunk row blocks (TSM2L, two stages per item) the plain loop (pipelining +25 %)
   if (dmma_ok) return split ? kDmmaP : kDmma;
-  // fp32 16-column passes: split-precision tf32 on the tensor cores (tsm2r_tc32.cuh; taken when
-  // the layout allows, else FFMA2): -13 % burst, -13 % sustained vs FFMA2 (profiles/envab_r01.json)
-  if (eb == 4 && nt == 16) return kTc;
+  // fp32 16-column passes with split row blocks (TSM2R): split-precision tf32 on the tensor cores
+  // (tsm2r_tc32.cuh; taken when the layout allows, else FFMA2): -13 % burst, -13 % sustained vs
+  // FFMA2 (profiles/envab_r01.json). Single-chunk row blocks (TSM2L) stay on FFMA2, whose
+  // direct-store epilogue streams C at 0.89 of the copy rate (2^24 x 16 x 16: 0.368 vs 0.597 ms
+  // sustained, profiles/tsm2l_fp32_r02.json)
+  if (eb == 4 && nt == 16) return split ? kTc : kFfma2;
   if (ffma2_ok) return kFfma2;
   return kFma;
 }
+
+// Whether an fp32 pass of width nt splits its row blocks into several column chunks (TSM2R) or
+// runs them as single chunks (TSM2L shapes), on the FFMA2 geometry (make_items below).
+static bool fp32_split(int sms, int64_t m, int64_t k, int nt);
 
 // fp32 split row blocks: the fp64 accumulator -> C pass, launched with programmatic dependent
 // launch so its launch latency hides behind the stream kernel's tail (the stream kernels trigger
@@ -568,6 +575,14 @@ static void make_items(int sms, int64_t m, int64_t k, size_t eb, int R, int KC, 
   }
   it->total = it->num_rb * it->nch();
   *grid = std::min<int64_t>(G_full, (it->total + it->batch - 1) / it->batch);
+}
+
+static bool fp32_split(int sms, int64_t m, int64_t k, int nt) {
+  using Cfg = TmaCfg<float, 16>;
+  Items it;
+  int64_t G;
+  make_items(sms, m, k, 4, Cfg::R, Cfg::KC, nt, current_tuning(), &it, &G);
+  return it.nch() > 1;
 }
 
 template <typename T, int NT, int KIND, int RPT, int CW, int SB = 32768>
@@ -1029,7 +1044,7 @@ static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m,
   if constexpr (sizeof(T) == 4 && (NT == 16 || NT == 8)) {
     // fp32: the tensor-core consumer when chosen (TSM2X_CONSUMER=tc / tuning consumer 4) and the
     // layout allows the 3-D TMA view; the deterministic (ordered) combine stays on FFMA2
-    if (tma && !ordered && pick_consumer_rt(4, NT, true, current_tuning()) == kTc &&
+    if (tma && !ordered && pick_consumer_rt(4, NT, fp32_split(di.sms, m, k, NT), current_tuning()) == kTc &&
         tc32_ok(reinterpret_cast<const float*>(A), m, k, lda))
       return run_tsm2r_tc32(di, ws, m, k, w, reinterpret_cast<const float*>(A), lda,
                             reinterpret_cast<const float*>(B), ldb, reinterpret_cast<float*>(C), ldc, c_is_zero, s);
@@ -1803,7 +1818,7 @@ int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, 
   const Tuning tu = current_tuning();
   Items it;
   int64_t G;
-  if (eb == 4 && nt == 16 && !determ && tu.combine != 1 && pick_consumer_rt(4, nt, true, tu) == kTc &&
+  if (eb == 4 && nt == 16 && !determ && tu.combine != 1 && pick_consumer_rt(4, nt, fp32_split(sms, m, k, nt), tu) == kTc &&
       a_aligned16 && lda % 4 == 0 && lda >= (int64_t)align_up((size_t)m, 32) && k < (int64_t(1) << 31)) {
     // fp32 16-column passes on the tensor cores (run_tsm2r_tc32)
     out->rows_per_block = Tc32Cfg::R;

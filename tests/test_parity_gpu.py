@@ -554,11 +554,20 @@ def test_run_native_multi_device_shards(devices):
 def test_tc32_tensor_core_shapes(c_zero):
     """fp32 16-column passes on the tensor cores (tsm2r_stream_tc32, split-precision tf32): ragged
     rows (m % 32, m % 512), ragged k (k % 16), n = 9..16, split and single-chunk row blocks,
-    C += A.B and the zero-C contract."""
+    C += A.B and the zero-C contract. Auto sends single-chunk row blocks to FFMA2, so the tensor
+    cores are forced (tuning consumer 4) to cover their single-chunk instantiation too."""
     import torch
     tsm = _tsm()
     from paper_2002_03258_b200 import tuning
     rng = np.random.default_rng(11 + c_zero)
+    tuning.set_tuning(tuning.Tuning(consumer=4))
+    try:
+        _tc32_shapes(tsm, tuning, rng, c_zero, torch)
+    finally:
+        tuning.set_tuning(None)
+
+
+def _tc32_shapes(tsm, tuning, rng, c_zero, torch):
     for (m, k, n) in [(1, 1, 16), (31, 7, 9), (33, 17, 12), (513, 100, 16), (4113, 5000, 16), (1024, 33, 15),
                       (70001, 16, 16), (2048, 40000, 16)]:
         assert tuning.plan("single", m, k, n)["consumer"] == "tc", (m, k, n)

@@ -79,6 +79,9 @@ def test_plan_fp32_and_wide():
     p = tuning.plan("single", 32768, 32768, 16)
     assert p["consumer"] == "tc" and p["t1"] == 512 and p["cols_per_stage"] == 16  # tcgen05 split tf32
     assert tuning.plan("single", 32768, 32768, 8)["consumer"] == "ffma2"
+    # TSM2L shapes (single-chunk row blocks): FFMA2 with direct stores, not the tensor cores
+    assert tuning.plan("single", 1 << 24, 16, 16)["consumer"] == "ffma2"
+    assert tuning.plan("single", 1 << 24, 16, 16)["nbig"] + tuning.plan("single", 1 << 24, 16, 16)["nsmall"] == 1
     p = tuning.plan("single", 32768, 32768, 16, deterministic=True)  # ordered combine stays on FFMA2
     assert p["consumer"] == "ffma2" and p["t1"] == 1024
     assert tuning.plan("single", 1001, 5000, 16, lda=1004)["consumer"] == "ffma2"  # lda < roundup(m, 32)

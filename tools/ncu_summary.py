@@ -20,7 +20,7 @@ OUT = os.path.join(ROOT, "profiles", "ncu_summary.json")
 
 KEYS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-    "gpc__cycles_elapsed.max.per_second", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "gpc__cycles_elapsed.max.per_second",
     "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__cycles_active.min", "sm__cycles_active.avg", "sm__cycles_active.max",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
