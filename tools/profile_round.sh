@@ -19,6 +19,6 @@ done
 for wl in tsm2r_fp64_n16 tsm2l_fp64 tsm2r_fp32_n16 tsm2r_fp64_n2 tsm2r_fp64_n4 tsm2r_fp64_n8_4096 tsm2r_fp64_n8_65536; do
   timeout 600 python bench.py --workload $wl --e2e-steps 2 --no-cpu-baseline >> gpurun_out/bench_${TAG}_other.jsonl 2>> gpurun_out/bench_${TAG}.err
 done
-timeout 600 python tools/ablation.py ${TAG} > gpurun_out/ablation_${TAG}.log 2>&1
+[ -n "$SKIP_ABLATION" ] || timeout 600 python tools/ablation.py ${TAG} > gpurun_out/ablation_${TAG}.log 2>&1
 cp profiles/ablation_${TAG}.json gpurun_out/ 2>/dev/null
 du -sh gpurun_out; ls -la gpurun_out
