@@ -6,6 +6,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -1281,6 +1283,77 @@ static bool is_pinned(const void* p) {
 }
 
 // host threads for the pageable staging copies and the zero-C scan
+// Persistent host worker pool for the host path's parallel copies and scans: a pageable 7.55 GB
+// A is staged as ~240 slabs of 32 MB, and spawning + joining 15 threads per slab (~0.3 ms) cost as
+// much as the copy itself. One parallel region at a time; a caller that finds the pool busy
+// (another device's host thread, tsm2x_run_host_multi) runs its region on fresh threads. The
+// pool is never destroyed (its workers are detached and live until the process exits).
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();
+    return *p;
+  }
+  // fn(t) for t in [0, nt): t = 0 on the calling thread, the others on the pool's workers
+  void run(unsigned nt, const std::function<void(unsigned)>& fn) {
+    std::unique_lock<std::mutex> busy(region_mu_, std::try_to_lock);
+    if (!busy.owns_lock() || nt > kMax) {
+      std::vector<std::thread> th;
+      for (unsigned t = 1; t < nt; ++t) th.emplace_back(fn, t);
+      fn(0);
+      for (auto& x : th) x.join();
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      while (workers_ + 1 < nt) {
+        std::thread(&HostPool::worker, this, workers_ + 1).detach();
+        ++workers_;
+      }
+      fn_ = &fn;
+      nt_ = nt;
+      pending_ = nt - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  static constexpr unsigned kMax = 64;
+  void worker(unsigned id) {
+    unsigned long long seen = 0;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      seen = gen_ - 1;  // a region may already be waiting for this new worker
+    }
+    for (;;) {
+      const std::function<void(unsigned)>* fn;
+      unsigned nt;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        fn = fn_;
+        nt = nt_;
+      }
+      if (fn && id < nt) {
+        (*fn)(id);
+        std::lock_guard<std::mutex> lk(mu_);
+        if (--pending_ == 0) done_cv_.notify_one();
+      }
+    }
+  }
+  std::mutex region_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(unsigned)>* fn_ = nullptr;
+  unsigned nt_ = 0, pending_ = 0, workers_ = 0;
+  unsigned long long gen_ = 0;
+};
+
 static unsigned host_threads(size_t bytes) {
   if (bytes < (8u << 20)) return 1;
   return std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
@@ -1312,10 +1385,7 @@ static bool host_all_zero(const T* C, int64_t m, int64_t n, int64_t ldc) {
           }
     }
   };
-  std::vector<std::thread> th;
-  for (unsigned t = 1; t < nt; ++t) th.emplace_back(scan, t);
-  scan(0);
-  for (auto& x : th) x.join();
+  HostPool::get().run(nt, scan);
   return !nonzero.load();
 }
 
@@ -1337,10 +1407,7 @@ static void par_copy2d(void* dst, size_t dpitch, const void* src, size_t spitch,
     work(0);
     return;
   }
-  std::vector<std::thread> th;
-  for (unsigned t = 1; t < nt; ++t) th.emplace_back(work, t);
-  work(0);
-  for (auto& x : th) x.join();
+  HostPool::get().run(nt, work);
 }
 
 // Per-device resources of the host path, kept across calls (allocation and stream creation
