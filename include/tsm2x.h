@@ -116,6 +116,25 @@ int tsm2x_run_host_multi(int variant, int precision, int64_t m, int64_t k, int64
                          const void* C_in, void* C_out, int64_t ldc,
                          const tsm2x_params* params, uint32_t flags, int ndev, const int* devices);
 
+/* Device-resident run over several GPUs of one process (the
+ * single-process form of the row sharding in multi.py). A and C are row-sharded: shard g holds
+ * rows [r0, r1) = tsm2x_row_range(m, ndev, g) as its own column-major block A[g] (lda[g]) and C[g]
+ * (ldc[g]) on devices[g] (a device may repeat). B (k x n, ldb) lives on devices[0]; each shard's
+ * stream waits for B on streams[0], every other device receives a copy over NVLink
+ * (cudaMemcpy3DPeerAsync into a per-(device, stream) buffer; peer access enabled once), and the
+ * shard runs as tsm2x_run on streams[g] (streams = NULL: every device's legacy default stream).
+ * No reduction: rows are independent (reference SPEC.md:262); each shard's rows are exactly what
+ * tsm2x_run on that shard alone returns (the column-chunk split of a row block follows the
+ * shard's size, so in general not the bits of the whole-matrix call, which is within the same
+ * tolerance). Asynchronous (stream-ordered per shard); restores the current device. */
+int tsm2x_run_multi(int variant, int precision, int64_t m, int64_t k, int64_t n, int ndev, const int* devices,
+                    const void* const* A, const int64_t* lda, const void* B, int64_t ldb, void* const* C,
+                    const int64_t* ldc, const tsm2x_params* params, uint32_t flags, void* const* streams);
+
+/* Row range [*r0, *r1) of shard g of an m-row problem over ndev shards: contiguous, balanced in
+ * 32-row units, the last shard takes the ragged tail (paper_2002_03258_b200.multi.row_partition). */
+void tsm2x_row_range(int64_t m, int ndev, int g, int64_t* r0, int64_t* r1);
+
 /* Frees the library's cached device memory on `device` (-1 = every device): the per-(device,
  * stream) workspaces (Bt, fp64 accumulators, queue counters; kept across calls and grown on
  * demand) and the host path's staging buffers, pinned buffers, events and streams. Synchronises

@@ -16,8 +16,10 @@ from .kernels import (  # noqa: F401
     colmajor_empty,
     fill_uniform,
     gemm,
+    gemm_multi,
     release_cached_memory,
     run_native,
+    row_range,
     run_native_multi,
     simulate,
 )
@@ -31,8 +33,10 @@ __all__ = [
     "colmajor_empty",
     "fill_uniform",
     "gemm",
+    "gemm_multi",
     "release_cached_memory",
     "run_native",
+    "row_range",
     "run_native_multi",
     "simulate",
     "validate_problem",

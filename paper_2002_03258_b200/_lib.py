@@ -24,6 +24,8 @@ EXPORTS = (
     "tsm2x_run_ex",
     "tsm2x_run_host",
     "tsm2x_run_host_multi",
+    "tsm2x_run_multi",
+    "tsm2x_row_range",
     "tsm2x_fill_uniform",
     "tsm2x_release_cached",
     "tsm2x_last_error",
@@ -85,6 +87,10 @@ def load() -> ctypes.CDLL:
         lib.tsm2x_run_host.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, vp, i64, pp, u32, i32]
         lib.tsm2x_run_host_multi.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, vp, i64, pp, u32, i32,
                                              ctypes.POINTER(ctypes.c_int)]
+        lib.tsm2x_run_multi.argtypes = [i32, i32, i64, i64, i64, i32, ctypes.POINTER(ctypes.c_int), vp,
+                                        ctypes.POINTER(i64), vp, i64, vp, ctypes.POINTER(i64), pp, u32, vp]
+        lib.tsm2x_row_range.argtypes = [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        lib.tsm2x_row_range.restype = None
         lib.tsm2x_fill_uniform.argtypes = [i32, i64, i64, vp, i64, i64, i64, ctypes.c_uint64, vp]
         lib.tsm2x_set_kernel_events.argtypes = [vp, vp]
         lib.tsm2x_set_tuning.argtypes = [ctypes.POINTER(Tuning)]
@@ -92,7 +98,7 @@ def load() -> ctypes.CDLL:
         lib.tsm2x_plan_for.argtypes = [i32, i64, i64, i64, i64, i32, u32, i32, ctypes.POINTER(Plan)]
         lib.tsm2x_release_cached.argtypes = [i32]
         for name in ("tsm2x_validate", "tsm2x_run", "tsm2x_run_ex", "tsm2x_run_host", "tsm2x_run_host_multi",
-                     "tsm2x_fill_uniform",
+                     "tsm2x_run_multi", "tsm2x_fill_uniform",
                      "tsm2x_version", "tsm2x_set_kernel_events", "tsm2x_set_tuning", "tsm2x_get_tuning",
                      "tsm2x_plan_for", "tsm2x_release_cached"):
             getattr(lib, name).restype = ctypes.c_int

@@ -187,6 +187,20 @@ __device__ __forceinline__ int64_t bt_index(int64_t row, int col, bool swz) {
   }
 }
 
+// Inline-B producer: a stage's "full" barrier completes on the TMA bytes plus the producer warp's
+// arrival after its B stores — lane 0's after __syncwarp in the production build; every lane's in
+// the racecheck build (compute-sanitizer racecheck does not follow the __syncwarp edge, see
+// common.cuh warp_release), whose barriers then count 32 arrivals.
+#ifdef TSM2X_RACECHECK
+constexpr int kInlineFullArrivals = 32;
+__device__ __forceinline__ void inline_publish(uint64_t* bar) { mbar_arrive(bar); }
+#else
+constexpr int kInlineFullArrivals = 1;
+__device__ __forceinline__ void inline_publish(uint64_t* bar) {
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
+#endif
+
 // Consumers that read B in DMMA fragment order (every DmmaConsumer, which declares kSwz).
 template <typename C, typename = void>
 struct FragOf : std::false_type {};
@@ -670,7 +684,7 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
         if (tl && threadIdx.x == 0) tl[0] = gtimer();)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], a.inline_b ? kInlineFullArrivals : 1);
       mbar_init(&empty[s], Cfg::CW * kArrivalsPerWarp);
     }
     mbar_fence_init();
@@ -731,6 +745,9 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
     while (have) {
       const int s = it % STAGES;
       const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+#ifdef TSM2X_RACECHECK
+      mbar_wait(&empty[s], ph ^ 1u);  // racecheck build: every lane acquires the slot it writes
+#endif
       if (lane == 0) {  // one lane polls (32 polling lanes would take smem cycles from the consumers)
         mbar_wait(&empty[s], ph ^ 1u);
         KDIAG(if (tl && it == 0) tl[1] = gtimer();)
@@ -752,7 +769,7 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
           if (idx < Cfg::B_ELEMS) dst[bt_index<NT, kFrag>(idx % KC, idx / KC, kSwzB)] = v[j];
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&full[prev_s]);
+        inline_publish(&full[prev_s]);
       }
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
@@ -782,13 +799,18 @@ __global__ void __launch_bounds__(Consumer::Cfg::THREADS, 1)
       }
     }
     __syncwarp();
-    if (lane == 0) {
-      if (prev_s >= 0) mbar_arrive(&full[prev_s]);
-      KDIAG(if (tl) tl[3] = gtimer();)
+    if (prev_s >= 0) inline_publish(&full[prev_s]);
+    {  // end-of-work marker for the consumers
       const int s = it % STAGES;
-      mbar_wait(&empty[s], ((uint32_t)(it / STAGES) & 1u) ^ 1u);
-      meta[s] = make_longlong2(-1, -1);
-      mbar_arrive(&full[s]);
+      if (lane == 0) {
+        KDIAG(if (tl) tl[3] = gtimer();)
+        mbar_wait(&empty[s], ((uint32_t)(it / STAGES) & 1u) ^ 1u);
+        meta[s] = make_longlong2(-1, -1);
+      }
+      __syncwarp();
+      inline_publish(&full[s]);
+    }
+    if (lane == 0) {
       __threadfence();
       const unsigned prev = atomicAdd(reinterpret_cast<unsigned*>(a.queue + 1), 1u);
       if (prev == gridDim.x - 1) {

@@ -1701,6 +1701,72 @@ __global__ void fill_uniform(T* p, int64_t rows, int64_t cols, int64_t ld, int64
   }
 }
 
+// tsm2x_run_multi: per-(device, stream) copies of B and peer access between the shard devices
+struct BCopy {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+static std::mutex g_bcopy_mu;
+static std::map<std::pair<int, cudaStream_t>, BCopy> g_bcopy;
+
+static int bcopy_reserve(int dev, cudaStream_t s, size_t bytes, void** out) {
+  std::lock_guard<std::mutex> lk(g_bcopy_mu);
+  BCopy& b = g_bcopy[{dev, s}];
+  if (bytes > b.cap) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    TSM2X_CUDA(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(TSM2X_EUNSUPPORTED, "B copy buffer must grow during a CUDA graph capture: make one eager call first");
+    if (b.p) TSM2X_CUDA(cudaFreeAsync(b.p, s));
+    b.p = nullptr;
+    b.cap = 0;
+    if (cudaMallocAsync(&b.p, bytes, s) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(TSM2X_ENOMEM, "B copy allocation of %zu bytes failed", bytes);
+    }
+    b.cap = bytes;
+  }
+  *out = b.p;
+  return TSM2X_OK;
+}
+
+static void bcopy_release(int device) {
+  std::lock_guard<std::mutex> lk(g_bcopy_mu);
+  for (auto it = g_bcopy.begin(); it != g_bcopy.end();) {
+    if (device < 0 || it->first.first == device) {
+      int prev = 0;
+      cudaGetDevice(&prev);
+      cudaSetDevice(it->first.first);
+      cudaDeviceSynchronize();
+      if (it->second.p) cudaFreeAsync(it->second.p, 0);  // stream-ordered allocation (bcopy_reserve)
+      cudaSetDevice(prev);
+      it = g_bcopy.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
+// enable access from `dev` (current device) to `peer` once; devices without a peer path fall back
+// to the driver's staged copy (cudaMemcpy3DPeerAsync handles both)
+static int peer_enable(int dev, int peer) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, bool> done;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(dev, peer);
+  if (done.count(key)) return TSM2X_OK;
+  int can = 0;
+  TSM2X_CUDA(cudaDeviceCanAccessPeer(&can, dev, peer));
+  if (can) {
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+      return fail(TSM2X_ECUDA, "cudaDeviceEnablePeerAccess(%d -> %d): %s", dev, peer, cudaGetErrorString(e));
+    cudaGetLastError();
+  }
+  done[key] = true;
+  return TSM2X_OK;
+}
+
 }  // namespace tsm2x
 
 // ============================================================================================
@@ -1774,6 +1840,74 @@ int tsm2x_run_host_multi(int variant, int precision, int64_t m, int64_t k, int64
   for (auto& x : th) x.join();
   for (int d = 0; d < ndev; ++d)
     if (rc[d] != TSM2X_OK) return fail(rc[d], "device %d: %s", devices[d], msg[d].c_str());
+  return TSM2X_OK;
+}
+
+void tsm2x_row_range(int64_t m, int ndev, int g, int64_t* r0, int64_t* r1) {
+  // contiguous row shards in 32-row units (paper_2002_03258_b200.multi.row_partition)
+  const int64_t blocks = (m + 31) / 32;
+  if (ndev < 1 || g < 0 || g >= ndev || m < 0) {
+    *r0 = *r1 = 0;
+    return;
+  }
+  *r0 = std::min<int64_t>(m, blocks * g / ndev * 32);
+  *r1 = std::min<int64_t>(m, blocks * (g + 1) / ndev * 32);
+}
+
+int tsm2x_run_multi(int variant, int precision, int64_t m, int64_t k, int64_t n, int ndev, const int* devices,
+                    const void* const* A, const int64_t* lda, const void* B, int64_t ldb, void* const* C,
+                    const int64_t* ldc, const tsm2x_params* params, uint32_t flags, void* const* streams) {
+  TSM2X_TRY(validate(variant, precision, m, k, n, params));
+  if (ndev < 1 || !devices) return fail(TSM2X_EINVAL, "need at least one device");
+  if (!A || !lda || !B || !C || !ldc) return fail(TSM2X_EINVAL, "null shard array or pointer");
+  const size_t eb = precision == TSM2X_DOUBLE ? 8 : 4;
+  int prev = 0;
+  TSM2X_CUDA(cudaGetDevice(&prev));
+  struct Restore {
+    int dev;
+    ~Restore() { cudaSetDevice(dev); }
+  } restore{prev};
+  auto stream_of = [&](int g) { return streams ? reinterpret_cast<cudaStream_t>(streams[g]) : (cudaStream_t)0; };
+  // B is ready on devices[0]'s stream: every shard's stream waits for it before reading or copying it
+  TSM2X_CUDA(cudaSetDevice(devices[0]));
+  cudaEvent_t b_ready;
+  TSM2X_CUDA(cudaEventCreateWithFlags(&b_ready, cudaEventDisableTiming));
+  struct EvDestroy {
+    cudaEvent_t e;
+    ~EvDestroy() { cudaEventDestroy(e); }  // safe once enqueued: released when the waits complete
+  } evd{b_ready};
+  TSM2X_CUDA(cudaEventRecord(b_ready, stream_of(0)));
+  for (int g = 0; g < ndev; ++g) {
+    int64_t r0, r1;
+    tsm2x_row_range(m, ndev, g, &r0, &r1);
+    if (r1 <= r0) continue;
+    const int dev = devices[g];
+    cudaStream_t sg = stream_of(g);
+    TSM2X_CUDA(cudaSetDevice(dev));
+    TSM2X_CUDA(cudaStreamWaitEvent(sg, b_ready, 0));
+    const void* Bg = B;
+    int64_t ldbg = ldb;
+    if (dev != devices[0]) {
+      // B (k x n) to this device once per call, over NVLink when the devices are peers (the 4 MB
+      // at configs[4] take microseconds); the copy lives in a per-(device, stream) buffer, so
+      // stream order makes its reuse by the next call on this stream safe
+      TSM2X_TRY(peer_enable(dev, devices[0]));
+      void* dst = nullptr;
+      TSM2X_TRY(bcopy_reserve(dev, sg, (size_t)k * n * eb, &dst));
+      cudaMemcpy3DPeerParms cp = {};
+      cp.srcPtr = make_cudaPitchedPtr(const_cast<void*>(B), (size_t)ldb * eb, (size_t)k * eb, (size_t)n);
+      cp.srcDevice = devices[0];
+      cp.dstPtr = make_cudaPitchedPtr(dst, (size_t)k * eb, (size_t)k * eb, (size_t)n);
+      cp.dstDevice = dev;
+      cp.extent = make_cudaExtent((size_t)k * eb, (size_t)n, 1);
+      TSM2X_CUDA(cudaMemcpy3DPeerAsync(&cp, sg));
+      Bg = dst;
+      ldbg = k;
+    }
+    const int rc = run_device_any(variant, precision, r1 - r0, k, n, A[g], lda[g], Bg, ldbg, C[g], ldc[g], params,
+                                  flags, TSM2X_IMPL_AUTO, sg);
+    if (rc != TSM2X_OK) return fail(rc, "shard %d (device %d): %s", g, dev, t_err);
+  }
   return TSM2X_OK;
 }
 
@@ -1918,6 +2052,7 @@ int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, 
 }
 
 int tsm2x_release_cached(int device) {
+  bcopy_release(device);  // tsm2x_run_multi's per-(device, stream) copies of B
   // per-(device, stream) workspaces: every stream that ever called the library on `device` (-1 =
   // all devices) — synchronised, then freed; the next call on a stream allocates afresh
   {

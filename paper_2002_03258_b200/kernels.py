@@ -173,6 +173,64 @@ def gemm(A, B, C, *, variant=Variant.V3, params=None, c_is_zero: bool = False, i
     return C
 
 
+def row_range(m: int, ndev: int, g: int):
+    """Rows [r0, r1) of shard ``g`` of an m-row problem over ``ndev`` shards (``tsm2x_row_range``:
+    contiguous, balanced in 32-row units — the same split as ``multi.row_partition``)."""
+    r0, r1 = ctypes.c_int64(), ctypes.c_int64()
+    _lib.load().tsm2x_row_range(int(m), int(ndev), int(g), ctypes.byref(r0), ctypes.byref(r1))
+    return r0.value, r1.value
+
+
+def gemm_multi(A_shards, B, C_shards, *, variant=Variant.V3, params=None, c_is_zero: bool = False,
+               deterministic: bool = False, streams=None):
+    """``gemm`` over several GPUs of this process (``tsm2x_run_multi``): ``A_shards[g]`` /
+    ``C_shards[g]`` are the rows ``row_range(m, len(A_shards), g)`` of A / C as column-major CUDA
+    tensors on their own devices (devices may repeat), B lives on ``A_shards[0]``'s device and
+    is copied to the other devices over NVLink inside the call; every shard is stream-ordered on
+    ``streams[g]`` (default: torch's current stream of its device). No reduction — rows are
+    independent (reference SPEC.md:262). Returns ``C_shards``."""
+    import torch
+    from .core import KernelParams
+    variant = Variant.coerce(variant)
+    nd = len(A_shards)
+    if nd < 1 or len(C_shards) != nd:
+        raise ValueError("need one A shard and one C shard per device")
+    dt = B.dtype
+    if dt not in (torch.float32, torch.float64) or any(t.dtype != dt for t in list(A_shards) + list(C_shards)):
+        raise ValueError("A, B, C must share one precision (float32 or float64)")
+    if not all(t.is_cuda for t in list(A_shards) + list(C_shards) + [B]):
+        raise ValueError("gemm_multi expects CUDA tensors")
+    k, n = B.shape
+    m = sum(int(a.shape[0]) for a in A_shards)
+    for g, (a, c) in enumerate(zip(A_shards, C_shards)):
+        r0, r1 = row_range(m, nd, g)
+        if a.shape != (r1 - r0, k) or c.shape != (r1 - r0, n) or a.device != c.device:
+            raise ValueError(f"shard {g}: expected A {r1 - r0}x{k} and C {r1 - r0}x{n} on one device "
+                             f"(rows {r0}:{r1} of {m}), got A {tuple(a.shape)} on {a.device}, "
+                             f"C {tuple(c.shape)} on {c.device}")
+    if B.device != A_shards[0].device:
+        raise ValueError("B must live on the first shard's device")
+    if params is None:
+        params = KernelParams(t1=128, t2=min(4, n), t3=4, tcf=1, variant=variant)
+    validate_params_for(params, m, k, n)
+    prec = _lib.DOUBLE if dt == torch.float64 else _lib.SINGLE
+    flags = (_lib.FLAG_C_IS_ZERO if c_is_zero else 0) | (_lib.FLAG_DETERMINISTIC if deterministic else 0)
+    if streams is None:
+        streams = [torch.cuda.current_stream(a.device) for a in A_shards]
+    i64 = ctypes.c_int64
+    devs = (ctypes.c_int * nd)(*[a.device.index for a in A_shards])
+    a_ptr = (ctypes.c_void_p * nd)(*[a.data_ptr() for a in A_shards])
+    c_ptr = (ctypes.c_void_p * nd)(*[c.data_ptr() for c in C_shards])
+    lda = (i64 * nd)(*[_ld(a, a.shape[0]) if a.shape[0] else 1 for a in A_shards])
+    ldc = (i64 * nd)(*[_ld(c, c.shape[0]) if c.shape[0] else 1 for c in C_shards])
+    st = (ctypes.c_void_p * nd)(*[s.cuda_stream for s in streams])
+    p = _params_struct(params)
+    rc = _lib.load().tsm2x_run_multi(variant.ordinal, prec, m, k, n, nd, devs, a_ptr, lda, B.data_ptr(), _ld(B, k),
+                                     c_ptr, ldc, ctypes.byref(p), flags, st)
+    _lib.check(rc)
+    return C_shards
+
+
 def fill_uniform(T, seed: int, row_offset: int = 0, col_offset: int = 0, stream=None):
     """Fills a column-major CUDA tensor with the counter-based U[0,1) generator (tsm2x.h)."""
     import torch

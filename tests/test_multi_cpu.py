@@ -117,3 +117,16 @@ def test_strong_split_equals_whole(tmp_path, world, m):
     for _ in range(steps):
         whole = naive_gemm(A, B, whole)
     assert np.array_equal(got, whole)
+
+
+def test_c_row_range_matches_row_partition():
+    """tsm2x_row_range (the C ABI's shard split for tsm2x_run_multi / tsm2x_run_host_multi) is
+    multi.row_partition, for ragged and tiny m."""
+    from paper_2002_03258_b200 import row_range
+    from paper_2002_03258_b200.multi import row_partition
+    for m in (0, 1, 31, 32, 33, 1000, 4099, 65536, 70001):
+        for nd in (1, 2, 3, 5, 8):
+            got = [row_range(m, nd, g) for g in range(nd)]
+            assert got == [row_partition(m, nd, g) for g in range(nd)], (m, nd)
+            assert got[0][0] == 0 and got[-1][1] == m
+    assert row_range(100, 2, 5) == (0, 0)  # out-of-range shard: empty

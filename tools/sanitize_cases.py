@@ -1,4 +1,4 @@
-"""Small calls through every kernel path, for compute-sanitizer (memcheck / racecheck / synccheck /
+"""Small calls through every kernel path (run with TSM2X_INLINE_B=0 and =1 to cover both B producers), for compute-sanitizer (memcheck / racecheck / synccheck /
 initcheck). Checks each result against a float64 torch reference so a sanitizer run is also a
 parity run. Usage (GPU box):
   compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_cases.py"""
@@ -11,6 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2002_03258_b200 as tsm  # noqa: E402
+from paper_2002_03258_b200 import tuning  # noqa: E402
 
 CASES = [
     # (m, k, n, dtype, kwargs)
@@ -21,7 +22,9 @@ CASES = [
     (3000, 16, 16, torch.float64, {"variant": "l-opt2", "c_is_zero": True}),  # TSM2L, single-chunk
     (2048, 1500, 8, torch.float64, {"deterministic": True}),                 # ordered tickets
     (2048, 1500, 16, torch.float32, {}),              # tcgen05 split tf32
-    (3000, 16, 16, torch.float32, {"variant": "l-opt2", "c_is_zero": True}),  # tc32 single-chunk (deferred epilogue)
+    (3000, 16, 16, torch.float32, {"variant": "l-opt2", "c_is_zero": True}),  # FFMA2 single-chunk, direct stores
+    (3000, 16, 16, torch.float32, {"variant": "l-opt2", "c_is_zero": True, "tc": True}),  # tc32 single-chunk (deferred epilogue)
+    (3000, 20, 16, torch.float32, {}),                # FFMA2 single-chunk, C += (4-column C groups)
     (2048, 1500, 8, torch.float32, {}),               # FFMA2
     (1000, 700, 40, torch.float64, {}),               # three passes (16 + 16 + 8)
     (777, 333, 8, torch.float64, {"impl": "ldg"}),    # LDG fallback
@@ -43,7 +46,13 @@ def main():
         else:
             tsm.fill_uniform(C, 3)
         ref = C.double() + A.double() @ B.double()
+        kw = dict(kw)
+        tc = kw.pop("tc", False)
+        if tc:  # force the tensor-core consumer (auto sends single chunks to FFMA2)
+            tuning.set_tuning(tuning.Tuning(consumer=4))
         tsm.gemm(A, B, C, **kw)
+        if tc:
+            tuning.set_tuning(None)
         torch.cuda.synchronize()
         err = ((C.double() - ref).norm() / ref.norm()).item()
         tol = 1e-12 if dt == torch.float64 else 1e-5
