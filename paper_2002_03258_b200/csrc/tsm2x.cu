@@ -8,6 +8,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <functional>
+#include <pthread.h>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -1291,8 +1292,14 @@ static bool is_pinned(const void* p) {
 class HostPool {
  public:
   static HostPool& get() {
-    static HostPool* p = new HostPool();
-    return *p;
+    static std::once_flag once;
+    std::call_once(once, [] {
+      instance() = new HostPool();
+      // a forked child has none of the parent's workers (and may inherit a locked mutex): it
+      // starts from a fresh pool (the old one is leaked)
+      pthread_atfork(nullptr, nullptr, [] { instance() = new HostPool(); });
+    });
+    return *instance();
   }
   // fn(t) for t in [0, nt): t = 0 on the calling thread, the others on the pool's workers
   void run(unsigned nt, const std::function<void(unsigned)>& fn) {
@@ -1324,6 +1331,10 @@ class HostPool {
 
  private:
   static constexpr unsigned kMax = 64;
+  static HostPool*& instance() {
+    static HostPool* p = nullptr;
+    return p;
+  }
   void worker(unsigned id) {
     unsigned long long seen = 0;
     {

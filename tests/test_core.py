@@ -185,3 +185,41 @@ def test_leading_dimension_rejects_overlapping_columns():
         _ld(overlap, 64)
     with pytest.raises(ValueError):
         _ld(torch.zeros(64, 8, dtype=torch.float64), 64)  # row-major
+
+
+@pytest.mark.filterwarnings("ignore:This process .* is multi-threaded:DeprecationWarning")
+def test_zero_c_scan_on_the_host_pool_and_after_fork():
+    """The L_OPT2 zero-C rule on a C large enough for the library's parallel host scan (its
+    persistent worker pool): ValueError with no device work, also in a forked child, which must
+    not wait for the parent's workers."""
+    D = tsm.Precision.DOUBLE
+    m, k, n = 1 << 17, 16, 16  # 16 MB of C: several scan threads
+    A, B = tsm.Matrix.zeros(m, k, D), tsm.Matrix.zeros(k, n, D)
+    Cv = np.zeros((m, n))
+    Cv[m - 1, n - 1] = 1.0  # the only nonzero, in the last thread's share
+    C = tsm.Matrix.from_2d(Cv, D)
+    p = tsm.KernelParams(t2=4, variant=tsm.Variant.L_OPT2)
+    for _ in range(3):
+        with pytest.raises(ValueError):
+            tsm.run_native(tsm.Variant.L_OPT2, A, B, C, p)
+    pid = os.fork()
+    if pid == 0:  # child: same check, exit code 0 iff ValueError
+        code = 1
+        try:
+            tsm.run_native(tsm.Variant.L_OPT2, A, B, C, p)
+        except ValueError:
+            code = 0
+        except BaseException:
+            code = 2
+        os._exit(code)
+    import time
+    deadline = time.time() + 60
+    while time.time() < deadline:
+        done, status = os.waitpid(pid, os.WNOHANG)
+        if done:
+            assert os.WIFEXITED(status) and os.WEXITSTATUS(status) == 0, status
+            return
+        time.sleep(0.05)
+    os.kill(pid, 9)
+    os.waitpid(pid, 0)
+    raise AssertionError("forked child hung in the host scan")
