@@ -218,7 +218,8 @@ static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t
 
 // ---- TMA descriptor for A (2-D: dim0 = rows, dim1 = columns; OOB elements read as zero)
 // Experiment knobs read once per process: TSM2X_L2POL (L2 policy of the A stream, policy_for) and
-// TSM2X_L2PROMO (tensor-map L2 promotion: 0, 64, 128, 256 bytes; default 256).
+// TSM2X_L2PROMO (tensor-map L2 promotion: 0, 64, 128, 256 bytes; default 128 — sustained A/B,
+// profiles/l2promo_r02.json: 256 B was 0.3-3.5 % slower on every workload, 0 / 64 / 128 tie).
 static int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
@@ -228,7 +229,7 @@ static int l2_policy() {
   return v;
 }
 static CUtensorMapL2promotion l2_promotion() {
-  static const int v = env_int("TSM2X_L2PROMO", 256);
+  static const int v = env_int("TSM2X_L2PROMO", 128);
   return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
          : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
          : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B

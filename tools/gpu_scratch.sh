@@ -1,2 +1,3 @@
-timeout 900 python tools/envab.py --cfg f16 --cands "base;TSM2X_CONSUMER=ffma2" --rounds 3 > gpurun_out/f16_ab.log 2>&1; tail -1 gpurun_out/f16_ab.log
-timeout 900 python tools/envab.py --cfg f8 --cands "base;TSM2X_CONSUMER=fma" --rounds 2 > gpurun_out/f8_ab.log 2>&1; tail -1 gpurun_out/f8_ab.log
+for cfg in r8 r16 l16 f16 r4 r2 l16f; do
+timeout 900 python tools/envab.py --cfg $cfg --cands "base;TSM2X_L2PROMO=128;TSM2X_L2PROMO=0;TSM2X_L2PROMO=64" --rounds 3 > gpurun_out/promo_$cfg.log 2>&1; tail -1 gpurun_out/promo_$cfg.log
+done
