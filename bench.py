@@ -19,7 +19,9 @@ runs at every N. Time = max over ranks of the device-event time of the K steps.
 Workloads whose A is under 4x the L2 (tsm2r_fp64_n8_4096) flush the L2 between steps and time
 each step with its own events.
 
-The JSON line also carries: roofline (dominant kernel, CUDA events around each launch),
+The JSON line also carries: roofline (dominant kernel; CUDA events bracketing each call's launches
+— prep_dyn when the call has one, the stream kernel, tsm2_finalize for fp32 split passes — so
+kernel_ms is the call's device time, a conservative denominator),
 cpu_baseline (the reference CPU path restated in numpy — oracle/ — on a bounded row sample, rank 0,
 N=1), e2e (same metric through the host-buffer C ABI tsm2x_run_host with pinned host buffers,
 H2D of A and D2H of C inside the timed region; at N=1 also e2e.drop_in: the reference user's call
@@ -385,9 +387,8 @@ def run_ours(args, wl):
             e.record(stream)
     # small problems (L2-flushed workloads) are shorter than the host's enqueue of one call: the
     # step is captured once as a CUDA graph and replayed, so the GPU never waits on Python between
-    # the flush and the step. The kernel-timing events go in a second graph (an event node between
-    # prep_dyn and the stream kernel would cut their programmatic-dependent-launch overlap), timed
-    # after the timed region under the same flush.
+    # the flush and the step. The call-timing events go in a second graph, timed after the timed
+    # region under the same flush, so the timed graph holds nothing but the call.
     graph = gtimed = None
     if flush and not distributed:
         gkev = mk()
@@ -410,16 +411,23 @@ def run_ours(args, wl):
     torch.cuda.synchronize()
     launches0 = _lib.launch_count()
     with ClockSampler(local) as clk:
+        if not flush:
+            # ~1 ms GPU spin before t0 (outside the timed region): the host enqueues the first steps
+            # while the GPU waits on it, so the K timed steps run back to back instead of the first
+            # one waiting for Python's first enqueue (a blocking-kernel start, as nvbench does)
+            torch.cuda._sleep(2_000_000)
         t0.record(stream)
         for i in range(args.steps):
             if flush:
                 torch.sum(scratch, dim=0, out=red)  # 252 MB read: evicts A from the 126 MB L2, leaves it clean
-            sevs[i][0].record(stream)
+            if flush:  # per-step events only where steps are timed one by one (flush in between)
+                sevs[i][0].record(stream)
             if graph is not None:
                 graph.replay()
             else:
-                step(kevs[i], bevs[i])
-            sevs[i][1].record(stream)
+                step(kevs[i], bevs[i] if distributed else None)  # broadcast events only where there is one
+            if flush:
+                sevs[i][1].record(stream)
         t1.record(stream)
         torch.cuda.synchronize()
     kern_list = []
@@ -440,6 +448,11 @@ def run_ours(args, wl):
     ms_total = sum(a_.elapsed_time(b_) for a_, b_ in sevs) if flush else t0.elapsed_time(t1)
     kern_ms = (sum(kern_list) if graph is not None else sum(a_.elapsed_time(b_) for a_, b_ in kevs)) / args.steps
     bcast_ms = sum(a_.elapsed_time(b_) for a_, b_ in bevs) / args.steps if distributed else 0.0
+    # device idle between consecutive steps (end of step i -> start of step i+1), and from t0 to the
+    # first step: evidence that the timed region is the steps back to back
+    gaps = [kevs[i][1].elapsed_time(kevs[i + 1][0]) for i in range(args.steps - 1)] if graph is None else []
+    step_gap_us = round(1000 * sum(gaps) / len(gaps), 2) if gaps else None
+    lead_us = round(1000 * t0.elapsed_time(kevs[0][0]), 2) if graph is None else None
     if distributed:
         t = torch.tensor([ms_total, kern_ms, bcast_ms], device=dev, dtype=torch.float64)
         if backend == "gloo":
@@ -495,8 +508,9 @@ def run_ours(args, wl):
             "data": "synthetic: counter-based U[0,1) generated on device (oracle/rng.py regenerates any slab)",
             "config": bench_config(wl, world),
             "timing": ("each step one CUDA-graph replay of the call (captured once), device events around it; "
-                       "kernel_ms from a second graph with events around the stream kernel" if graph is not None
+                       "kernel_ms from a second graph with events around the call" if graph is not None
                        else "device events around the K eagerly enqueued steps"),
+            "step_gap_us": step_gap_us, "lead_us": lead_us,
             "GBps": round(gbps, 1),
             "roofline": {"bound": "hbm", "achieved": round(kern_gbps, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(kern_gbps / peak, 4), "traffic": traffic,

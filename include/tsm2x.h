@@ -185,9 +185,12 @@ typedef struct tsm2x_plan {
 int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, int a_aligned16, uint32_t flags,
                    int impl, tsm2x_plan* out);
 
-/* Profiling hook (bench evidence): the NEXT main kernel launched by this thread (the TSM2R
- * stream kernel or the TSM2L kernel of the next run call) is bracketed by cudaEventRecord of
- * these two cudaEvent_t on its stream; the hook then clears. Pass NULLs to clear explicitly. */
+/* Profiling hook (bench evidence): the NEXT device-resident call made by this thread
+ * (tsm2x_run / tsm2x_run_ex) is bracketed by cudaEventRecord of these two cudaEvent_t on its
+ * stream — before its first launch (prep_dyn, when the call has one) and after its last (the
+ * stream kernel, or tsm2_finalize for fp32 split passes), so the events never sit inside the
+ * programmatic-dependent-launch chain between those kernels; the hook then clears. Pass NULLs to
+ * clear explicitly. */
 int tsm2x_set_kernel_events(void* start_event, void* stop_event);
 
 /* Thread-local message describing the last non-OK return on this thread. */

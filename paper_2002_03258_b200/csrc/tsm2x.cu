@@ -708,16 +708,15 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
     zrows = m;
   }
   // inline B (no prep kernel, the producer warp gathers each stage's Bt rows from B itself):
-  // taken when there is nothing to zero and either the call is small (A <= 256 MB: one launch
-  // per call instead of two, BASELINE configs[0] 30.3 -> 28.6 us) or the pass is the fp64 DMMA
-  // 8-column tile (n = 3..8: -1.9 to -2.2 % sustained at 30720^2). Wider / FMA passes keep prep:
-  // the per-stage gather costs shared-memory cycles at n = 16 (+3.5 %) and L2 latency in the
-  // producer loop on the short 32 KB stages of n = 2 (+9 %) (profiles/inline_b_r02.json).
+  // taken when there is nothing to zero and the call is small (A <= 256 MB: one launch per call
+  // instead of two, BASELINE configs[0] 30.3 -> 28.6 us). Large calls keep prep_dyn: the
+  // per-stage gather costs ~1 % of the stream kernel at n = 8 in burst runs (1.0365 vs 1.0288
+  // ms per call, one box, profiles/inline_b_r02.json) and more at n = 16 / on 32 KB stages; only
+  // deep in the power-capped regime (> 1 s back to back) is it ~2 % ahead at n = 3..8.
   // TSM2X_INLINE_B = 0 never, 1 always, unset = this rule.
   static const int inline_env = env_int("TSM2X_INLINE_B", -1);
-  const bool frag8 = sizeof(T) == 8 && NT == 8 && (kind == kDmma || kind == kDmmaP);
   const bool want_inline =
-      inline_env == 1 || (inline_env < 0 && ((double)m * (double)k * (double)eb <= 256.0 * 1048576.0 || frag8));
+      inline_env == 1 || (inline_env < 0 && (double)m * (double)k * (double)eb <= 256.0 * 1048576.0);
   if (!zp && want_inline) {
     a.inline_b = 1;
     a.B = B;
@@ -757,8 +756,6 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
     TSM2X_TRY(encode_a_map_swz(&tmap, reinterpret_cast<const double*>(A), m, k, lda, Cfg::KC, Cfg::R));
   else
     TSM2X_TRY(encode_a_map(&tmap, A, m, k, lda, eb, Cfg::BOX, Cfg::KC));
-  const bool timed = t_ev_start && t_ev_stop;
-  if (timed) TSM2X_CUDA(record_kernel_event(t_ev_start, s));
   if (swz && kind == kDmma)
     TSM2X_TRY((launch_tma_kernel<T, NT, kDmmaS, RPT, CW, SB>(a, tmap, G, s)));
   else if (swz && kind == kDmmaP)
@@ -799,10 +796,6 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
             med[4], mx[4], (long long)G);
   }
 #endif
-  if (timed) {
-    TSM2X_CUDA(record_kernel_event(t_ev_stop, s));
-    t_ev_start = t_ev_stop = nullptr;
-  }
   if (atomic_split && sizeof(T) == 4) {
     const int64_t tot = m * w;
     const unsigned grid = (unsigned)std::min<int64_t>((tot + 255) / 256, (int64_t)di.sms * 8);
@@ -873,8 +866,6 @@ static int run_tsm2r_tc32(const DevInfo& di, Workspace* ws, int64_t m, int64_t k
   TSM2X_TRY(encode_a_map_tc32(&tmap, A, m, k, lda));
   auto kern = split ? tsm2r_stream_tc32<false> : tsm2r_stream_tc32<true>;
   TSM2X_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  const bool timed = t_ev_start && t_ev_stop;
-  if (timed) TSM2X_CUDA(record_kernel_event(t_ev_start, s));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)G);
   cfg.blockDim = dim3(Cfg::THREADS);
@@ -897,10 +888,6 @@ static int run_tsm2r_tc32(const DevInfo& di, Workspace* ws, int64_t m, int64_t k
             "\"mma_wait_acc\": %.0f, \"conv_wait_full\": %.0f, \"conv_wait_lo_empty\": %.0f, \"conv_convert\": %.0f, "
             "\"conv_epilogue\": %.0f}\n",
             env_diag & 0xffff, h[4], h[0] / ns, h[1] / ns, h[2] / ns, h[3] / ns, h[8] / ns, h[9] / ns, h[10] / ns, h[11] / ns);
-  }
-  if (timed) {
-    TSM2X_CUDA(record_kernel_event(t_ev_stop, s));
-    t_ev_start = t_ev_stop = nullptr;
   }
   if (split) {
     const int64_t tot = m * w;
@@ -947,15 +934,9 @@ static int run_tsm2r_tma_static(const DevInfo& di, Workspace* ws, int64_t m, int
   a.counters = ws->counters + 4;
   alignas(64) CUtensorMap tmap;
   TSM2X_TRY(encode_a_map(&tmap, A, m, k, lda, sizeof(T), Cfg::BOX, Cfg::KC));
-  const bool timed = t_ev_start && t_ev_stop;
-  if (timed) TSM2X_CUDA(record_kernel_event(t_ev_start, s));
   void* args[] = {&a, &tmap};
   TSM2X_CUDA(cudaLaunchKernel((const void*)kern, dim3((unsigned)G), dim3(Cfg::THREADS), args, Cfg::SMEM, s));
   TSM2X_TRY(check_launch("tsm2r_static_tma"));
-  if (timed) {
-    TSM2X_CUDA(record_kernel_event(t_ev_stop, s));
-    t_ev_start = t_ev_stop = nullptr;
-  }
   if (a.defer) {
     dim3 grid((unsigned)((Cfg::R + 255) / 256), (unsigned)a.num_rb);
     reduce_partials<T, NT, Cfg::R><<<grid, 256, 0, s>>>(a);
@@ -1008,15 +989,9 @@ static int run_tsm2r_ldg(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   a.Bt = Bt;
   a.ws = reinterpret_cast<T*>(rest);
   a.counters = ws->counters + 4;
-  const bool timed = t_ev_start && t_ev_stop;
-  if (timed) TSM2X_CUDA(record_kernel_event(t_ev_start, s));
   void* args[] = {&a};
   TSM2X_CUDA(cudaLaunchKernel(kfn, dim3((unsigned)G), dim3(THREADS), args, 0, s));
   TSM2X_TRY(check_launch("tsm2r_stream_ldg"));
-  if (timed) {
-    TSM2X_CUDA(record_kernel_event(t_ev_stop, s));
-    t_ev_start = t_ev_stop = nullptr;
-  }
   if (a.defer) {
     dim3 grid((unsigned)((R + 255) / 256), (unsigned)a.num_rb);
     if (R == 256)
@@ -1127,14 +1102,8 @@ static int run_tsm2l_pass(const DevInfo& di, int64_t m, int64_t k, int w, const 
   int64_t grid = std::min<int64_t>((groups + THREADS - 1) / THREADS, (int64_t)di.sms * occ);
   grid = std::max<int64_t>(grid, 1);
   void* args[] = {&a};
-  const bool timed = t_ev_start && t_ev_stop;
-  if (timed) TSM2X_CUDA(record_kernel_event(t_ev_start, s));
   TSM2X_CUDA(cudaLaunchKernel(kfn, dim3((unsigned)grid), dim3(THREADS), args, 0, s));
   TSM2X_TRY(check_launch("tsm2l"));
-  if (timed) {
-    TSM2X_CUDA(record_kernel_event(t_ev_stop, s));
-    t_ev_start = t_ev_stop = nullptr;
-  }
   return TSM2X_OK;
 }
 
@@ -1165,14 +1134,8 @@ static int run_tsm2l_splitn_pass(const DevInfo& di, int64_t m, int64_t k, int w,
     const int64_t groups = (m + Vec<T>::N - 1) / Vec<T>::N;
     int64_t grid = std::min<int64_t>((groups + THREADS / S - 1) / (THREADS / S), (int64_t)di.sms * occ);
     grid = std::max<int64_t>(grid, 1);
-    const bool timed = t_ev_start && t_ev_stop;
-    if (timed) TSM2X_CUDA(record_kernel_event(t_ev_start, s));
     kern<<<(unsigned)grid, THREADS, 0, s>>>(a);
     TSM2X_TRY(check_launch("tsm2l_splitn"));
-    if (timed) {
-      TSM2X_CUDA(record_kernel_event(t_ev_stop, s));
-      t_ev_start = t_ev_stop = nullptr;
-    }
     return TSM2X_OK;
   }
 }
@@ -1190,6 +1153,10 @@ __global__ void nonzero_check(const T* __restrict__ C, int64_t m, int64_t n, int
 }
 
 // ---- one full device-resident call ----------------------------------------------------------
+template <typename T>
+static int run_passes(int variant, int64_t m, int64_t k, int64_t n, const T* A, int64_t lda, const T* B,
+                      int64_t ldb, T* C, int64_t ldc, const tsm2x_params* params, uint32_t flags, int impl,
+                      bool c_is_zero, const DevInfo& di, Workspace* ws, cudaStream_t s);
 template <typename T>
 static int run_device(int variant, int64_t m, int64_t k, int64_t n, const T* A, int64_t lda, const T* B, int64_t ldb,
                       T* C, int64_t ldc, const tsm2x_params* params, uint32_t flags, int impl, cudaStream_t s) {
@@ -1215,6 +1182,22 @@ static int run_device(int variant, int64_t m, int64_t k, int64_t n, const T* A, 
     if (h) return fail(TSM2X_EINVAL, "L_OPT2 stores partial sums to C and requires a zeroed C");
     c_is_zero = true;
   }
+  // tsm2x_set_kernel_events: the two events bracket the whole call — its first launch (prep_dyn
+  // when there is one) to its last (tsm2_finalize for fp32 split passes) — so they sit outside
+  // the programmatic-dependent-launch chain between those kernels instead of cutting it
+  const cudaEvent_t ev0 = t_ev_start, ev1 = t_ev_stop;
+  t_ev_start = t_ev_stop = nullptr;
+  const bool timed = ev0 && ev1;
+  if (timed) TSM2X_CUDA(record_kernel_event(ev0, s));
+  TSM2X_TRY(run_passes<T>(variant, m, k, n, A, lda, B, ldb, C, ldc, params, flags, impl, c_is_zero, di, ws, s));
+  if (timed) TSM2X_CUDA(record_kernel_event(ev1, s));
+  return TSM2X_OK;
+}
+
+template <typename T>
+static int run_passes(int variant, int64_t m, int64_t k, int64_t n, const T* A, int64_t lda, const T* B,
+                      int64_t ldb, T* C, int64_t ldc, const tsm2x_params* params, uint32_t flags, int impl,
+                      bool c_is_zero, const DevInfo& di, Workspace* ws, cudaStream_t s) {
   if (impl == TSM2X_IMPL_ABLATION) {
     if (variant > TSM2X_V2) impl = TSM2X_IMPL_AUTO;
     else return run_ablation<T>(variant, m, k, n, A, lda, B, ldb, C, ldc, params, c_is_zero, s);

@@ -45,7 +45,7 @@ def test_default_bench_line():
     d = _last_json(out.stdout)
     for key in REQUIRED + ["roofline", "cpu_baseline", "e2e", "clocks", "gpu_launches"]:
         assert key in d, key
-    assert d["gpu_launches"] == 20  # one stream-kernel launch per step (inline B: no prep kernel at n=8)
+    assert d["gpu_launches"] == 40  # prep_dyn + the stream kernel per step (large call: B staged by prep)
     r = d["roofline"]
     assert r["bound"] == "hbm" and 0.5 < r["frac"] < 1.3
     assert d["e2e"]["h2d_bytes_per_step"] > 7e9

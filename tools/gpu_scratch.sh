@@ -1,3 +1,4 @@
-timeout 900 python tools/envab.py --cfg r8 --cands "base;TSM2X_L2POL=1;TSM2X_L2POL=2;TSM2X_L2POL=3;ENVAB_TUNING=tail_pct=30;ENVAB_TUNING=big_kb=8192" --rounds 3 > gpurun_out/r8_pol.log 2>&1; tail -1 gpurun_out/r8_pol.log
-timeout 900 python tools/envab.py --cfg l16 --cands "base;TSM2X_L2POL=1;ENVAB_TUNING=batch_kb=512;ENVAB_TUNING=batch_kb=2048" --rounds 3 > gpurun_out/l16_pol.log 2>&1; tail -1 gpurun_out/l16_pol.log
-timeout 900 python tools/envab.py --cfg r2 --cands "base;TSM2X_INLINE_B=1;TSM2X_STAGE_KB=64" --rounds 3 > gpurun_out/r2_pol.log 2>&1; tail -1 gpurun_out/r2_pol.log
+for r in 1 2; do for e in "" "TSM2X_INLINE_B=0"; do
+env $e python bench.py --steps 20 --warmup 5 --e2e-steps 0 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$e', d['ms_per_step'], d['roofline']['kernel_ms'], d['step_gap_us'], d['lead_us'], d['gpu_launches'])"
+done; done
+python bench.py --workload tsm2r_fp64_n8_4096 --steps 50 --warmup 5 --e2e-steps 0 --no-cpu-baseline 2>/dev/null | tail -1 | cut -c1-300
