@@ -3,6 +3,7 @@
 // / without the prep kernel asking for the max-shared carveout). Event-timed, back to back and
 // isolated. Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/launch_probe tools/launch_probe.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __global__ void k_big(int* p, int pdl) {
@@ -54,11 +55,12 @@ static float run(int mode, int reps, bool iso, int* d, size_t smem) {
   return tot * 1000.f / reps;
 }
 
-int main() {
+int main(int argc, char** argv) {
   setvbuf(stdout, nullptr, _IONBF, 0);
   int* d;
   cudaMalloc(&d, 1 << 24);
-  const size_t smem = 200 * 1024;
+  const size_t smem = (argc > 1 ? atoi(argv[1]) : 200) * 1024;  // dynamic smem of the big kernel, KB
+  printf("big kernel: 148 CTAs x 288 threads, %zu KB dynamic shared memory\n", smem / 1024);
   cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const char* names[] = {"big alone", "prep + big", "prep(carveout 100) + big", "prep + big (PDL)",
                          "prep(carveout 100) + big (PDL)"};
