@@ -132,7 +132,7 @@ def _copy_flat(storage, dtype) -> np.ndarray:
     out = np.empty(src.size, dtype=dtype)
     import os
     from concurrent.futures import ThreadPoolExecutor
-    nt = max(1, min(8, os.cpu_count() or 1))
+    nt = max(1, min(16, os.cpu_count() or 1))
     cuts = [src.size * i // nt for i in range(nt + 1)]
     with ThreadPoolExecutor(nt) as pool:
         list(pool.map(lambda i: np.copyto(out[cuts[i]:cuts[i + 1]], src[cuts[i]:cuts[i + 1]]), range(nt)))

@@ -1,1 +1,1 @@
-CANDS="base;TSM2X_STAGE_KB=32;TSM2X_CONSUMER=fma;TSM2X_CONSUMER=dmma;TSM2X_SWZ=0" bash tools/burst_ab.sh
+python tools/matrix_copy_probe.py
