@@ -25,10 +25,10 @@
 // prep_tc32, one 2 KB block per stage, bulk-copied next to the A stage. lo(A) sits in TMEM as
 // 128 lanes (rows) x 16 columns (K) per tile.
 //
-// Roles (320 threads, one CTA per SM): warp 0 producer (same dynamic item queue and order as
-// tsm2r_stream_tma), warp 1 TMEM allocator + MMA issuer (one lane), warps 2-9 converters and
+// Roles (576 threads, one CTA per SM): warp 0 producer (same dynamic item queue and order as
+// tsm2r_stream_tma), warp 1 TMEM allocator + MMA issuer (one lane), warps 2-17 converters and
 // epilogue. Converter warp w handles TMEM lane quarter w % 4 (the only lanes it may touch) of
-// tiles {2h, 2h + 1}, h = (w - 2) / 4. Pipelines: full/empty (TMA <-> MMA, empty released by
+// tile (w - 2) / 4 (with -DTSM2X_TC32_CW=8: 320 threads, warps 2-9, tiles {2h, 2h + 1}). Pipelines: full/empty (TMA <-> MMA, empty released by
 // tcgen05.commit), lo_full (converters -> MMA, 4 TMEM slots: the converters run up to four stages
 // ahead of the tensor core; a slot is reused once the stage four back has released its smem
 // stage), acc_full/acc_empty (MMA <-> converters, 2 accumulator buffers alternating per segment;
@@ -58,7 +58,14 @@ struct Tc32Cfg {
   static constexpr int STAGES = 6;
   static constexpr int A_BYTES = R * KC * 4;
   static constexpr int B_BYTES = 32 * KC * 4;  // [B | lo(B)] K-major, 2 KB
-  static constexpr int CONV_WARPS = 8;
+  // converter warps: 16 (one 128-row tile per warp; default: -0.45 % burst, -0.6 % sustained at
+  // configs[3] vs 8 warps of two tiles, profiles/tc32_cw_r02.json) or 8 (-DTSM2X_TC32_CW=8)
+#ifndef TSM2X_TC32_CW
+#define TSM2X_TC32_CW 16
+#endif
+  static constexpr int CONV_WARPS = TSM2X_TC32_CW;
+  static constexpr int TPW = TILES * 4 / CONV_WARPS;  // tiles per converter warp (a warp owns one TMEM lane quarter)
+  static_assert(TPW >= 1 && TPW * CONV_WARPS == TILES * 4, "converter warps cover every (tile, lane quarter)");
   // accumulation segment: the tensor core's fp32 accumulation (not round-to-nearest: 2048-column
   // chains measured 2.5e-5 relative at K = 32768) is drained into fp64 every SEG stages
   static constexpr int SEG = 8;
@@ -356,16 +363,16 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
     pdl_wait();
     const int cw = warp - 2;        // 0..7
     const int q = warp & 3;         // TMEM lane quarter this warp may access
-    const int t0 = 2 * (cw >> 2);   // tiles t0, t0 + 1
+    const int t0 = Cfg::TPW * (cw >> 2);  // tiles t0 .. t0 + TPW - 1
     const uint32_t lane_addr = (uint32_t)(32 * q) << 16;
     int64_t cur = -1, cur_rb = 0;
     int left = 0;                      // stages of the current item still to come
     int seg = -1, pend = -1, sin = 0;  // current segment, segment awaiting its drain, stages in segment
     // this thread's row of tiles t0, t0 + 1: running sums of the drained segments (fp32 with
     // round-to-nearest over ~16 segment values; fp64 would not fit the 168-register budget)
-    float sum[2][16];
+    float sum[Cfg::TPW][16];
 #pragma unroll
-    for (int tt = 0; tt < 2; ++tt)
+    for (int tt = 0; tt < Cfg::TPW; ++tt)
 #pragma unroll
       for (int j = 0; j < 16; ++j) sum[tt][j] = 0.f;
     TC32_DIAG(unsigned long long c_full = 0, c_loe = 0, c_conv = 0, c_epi = 0;)
@@ -374,7 +381,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
       mbar_wait_sleep(&acc_full[g & 1], (uint32_t)(g >> 1) & 1u);
       tc_fence_after();
 #pragma unroll
-      for (int tt = 0; tt < 2; ++tt) {
+      for (int tt = 0; tt < Cfg::TPW; ++tt) {
         const uint32_t base = tmem + lane_addr + (uint32_t)((g & 1) * Cfg::BUF_COLS + (t0 + tt) * Cfg::ACC_COLS);
         uint32_t dh[16], dl[16];
         tmem_ld16(base, dh);       // A x B + lo(A) x B
@@ -400,7 +407,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
       drain(fin_seg);
       const int64_t nch = a.it.nch();
 #pragma unroll
-      for (int tt = 0; tt < 2; ++tt) {
+      for (int tt = 0; tt < Cfg::TPW; ++tt) {
         const int64_t row = fin_rb * R + (t0 + tt) * 128 + 32 * q + lane;
         if (row < a.m) {
 #pragma unroll
@@ -467,7 +474,7 @@ __global__ void __launch_bounds__(Tc32Cfg::THREADS, 1)
       tc_fence_after();
       const unsigned char* st = sA + (size_t)s * Cfg::A_BYTES;
 #pragma unroll
-      for (int tt = 0; tt < 2; ++tt) {
+      for (int tt = 0; tt < Cfg::TPW; ++tt) {
         const int t = t0 + tt;
         // row 128t + 32q + lane lives in 32-row chunk 4t + q; column k at (k/4)*512 + (k%4)*128,
         // 32-byte unit (lane/8) ^ (k%4), word lane%8
