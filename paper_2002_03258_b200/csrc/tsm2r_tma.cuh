@@ -451,9 +451,11 @@ struct Ffma2Consumer {
 // the smem pipe 83 % busy). With the swizzle and the k-step's four columns taken as
 // {0, 2, 4, 6} / {1, 3, 5, 7} of each 8-column group (B's fragment order permuted to match,
 // prep_dyn), a phase's eight pieces land on eight distinct positions.
-template <int NT, int CW_ = 8, bool PIPE_ = false, int SB_ = 32768, bool SWZ_ = false>
+template <int NT, int CW_ = 8, bool PIPE_ = false, int SB_ = 32768, bool SWZ_ = false, int RB_ = 512>
 struct DmmaConsumer {
-  using Cfg = TmaCfg<double, NT, 16 / CW_, CW_, SB_>;  // R = 512 rows for CW_ in {8, 16}
+  // R = RB_ rows per row block: 512 (CW_ = 8 warps x 64 rows, or 16 x 32), or 1024 (16 warps x
+  // 64 rows; TSM2X_RB=1024 experiment: 8 KB contiguous per column per stage)
+  using Cfg = TmaCfg<double, NT, RB_ / (32 * CW_), CW_, SB_>;
   static constexpr bool kFragB = true;
   static constexpr bool kSwz = SWZ_;
   static_assert(!SWZ_ || Cfg::KC % 8 == 0, "swizzled layout: whole 8-column groups per stage");

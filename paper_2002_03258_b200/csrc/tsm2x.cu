@@ -593,28 +593,41 @@ template <typename T, int NT, int KIND, int RPT, int CW, int SB = 32768>
 struct ConsumerFor {
   using type = FmaConsumer<T, NT, RPT, CW, SB>;
 };
+// DMMA geometries: 512-row blocks (RPT * CW == 16: 8 warps x 64 rows or 16 x 32) or 1024-row
+// blocks (16 warps x 64 rows, RPT = 2); swizzled variants need 64 KB stages and 64 rows per warp
+template <int RPT, int CW, int SB>
+struct DmmaGeom {
+  static constexpr int R = 32 * RPT * CW;
+  // 1024-row blocks only with 64 KB stages (8 columns: two 4-column k-steps for the pipelined loop)
+  static constexpr bool ok = (RPT * CW == 16 && (CW == 8 || CW == 16)) || (RPT * CW == 32 && CW == 16 && SB == 65536);
+  static constexpr bool swz_ok = ok && R / CW == 64 && SB == 65536;
+};
 template <int NT, int RPT, int CW, int SB>
 struct ConsumerFor<double, NT, kDmma, RPT, CW, SB> {
-  using type = typename std::conditional<((NT == 8 || NT == 16) && RPT * CW == 16 && (CW == 8 || CW == 16)),
-                                         DmmaConsumer<(NT >= 8 ? NT : 8), (CW == 16 ? 16 : 8), false, SB>,
+  using type = typename std::conditional<((NT == 8 || NT == 16) && DmmaGeom<RPT, CW, SB>::ok && (CW == 8 || CW == 16)),
+                                         DmmaConsumer<(NT >= 8 ? NT : 8), (CW == 16 ? 16 : 8), false, SB, false,
+                                                      DmmaGeom<RPT, CW, SB>::R>,
                                          FmaConsumer<double, NT, RPT, CW, SB>>::type;
 };
 template <int NT, int RPT, int CW, int SB>
 struct ConsumerFor<double, NT, kDmmaP, RPT, CW, SB> {
-  using type = typename std::conditional<((NT == 8 || NT == 16) && RPT * CW == 16 && (CW == 8 || CW == 16)),
-                                         DmmaConsumer<(NT >= 8 ? NT : 8), (CW == 16 ? 16 : 8), true, SB>,
+  using type = typename std::conditional<((NT == 8 || NT == 16) && DmmaGeom<RPT, CW, SB>::ok && (CW == 8 || CW == 16)),
+                                         DmmaConsumer<(NT >= 8 ? NT : 8), (CW == 16 ? 16 : 8), true, SB, false,
+                                                      DmmaGeom<RPT, CW, SB>::R>,
                                          FmaConsumer<double, NT, RPT, CW, SB>>::type;
 };
 template <int NT, int RPT, int CW, int SB>
 struct ConsumerFor<double, NT, kDmmaS, RPT, CW, SB> {
-  using type = typename std::conditional<((NT == 8 || NT == 16) && RPT * CW == 16 && CW == 8 && SB == 65536),
-                                         DmmaConsumer<(NT >= 8 ? NT : 8), 8, false, 65536, true>,
+  using type = typename std::conditional<((NT == 8 || NT == 16) && DmmaGeom<RPT, CW, SB>::swz_ok && SB == 65536),
+                                         DmmaConsumer<(NT >= 8 ? NT : 8), (CW == 16 ? 16 : 8), false, 65536, true,
+                                                      DmmaGeom<RPT, CW, SB>::R>,
                                          FmaConsumer<double, NT, RPT, CW, SB>>::type;
 };
 template <int NT, int RPT, int CW, int SB>
 struct ConsumerFor<double, NT, kDmmaPS, RPT, CW, SB> {
-  using type = typename std::conditional<((NT == 8 || NT == 16) && RPT * CW == 16 && CW == 8 && SB == 65536),
-                                         DmmaConsumer<(NT >= 8 ? NT : 8), 8, true, 65536, true>,
+  using type = typename std::conditional<((NT == 8 || NT == 16) && DmmaGeom<RPT, CW, SB>::swz_ok && SB == 65536),
+                                         DmmaConsumer<(NT >= 8 ? NT : 8), (CW == 16 ? 16 : 8), true, 65536, true,
+                                                      DmmaGeom<RPT, CW, SB>::R>,
                                          FmaConsumer<double, NT, RPT, CW, SB>>::type;
 };
 template <typename T, int NT, int RPT, int CW, int SB>
@@ -682,12 +695,12 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   const size_t acc_bytes = (atomic_split && sizeof(T) == 4) ? (size_t)a.ldacc * NT * sizeof(double) : 0;
   int kind = pick_consumer_rt(sizeof(T), NT, split, tu);
   // DMMA: the 512-row geometries (8 warps x 2 rows or 16 warps x 1 row); FFMA2: the default one
-  if ((kind == kDmma || kind == kDmmaP) && !(RPT * CW == 16 && (CW == 8 || CW == 16))) kind = kFma;
+  if ((kind == kDmma || kind == kDmmaP) && !DmmaGeom<RPT, CW, SB>::ok) kind = kFma;
   if (kind == kFfma2 && (RPT != Vec<T>::N || CW != 8 || SB != 32768)) kind = kFma;
   if (kind == kTc) kind = (sizeof(T) == 4 && RPT == Vec<T>::N && CW == 8 && NT >= 2) ? kFfma2 : kFma;  // tc path not taken
   // the default DMMA geometry reads A through the swizzled layout when the leading dimension
   // allows it (bank-conflict-free fragment loads; DmmaConsumer)
-  const bool swz = sizeof(T) == 8 && (kind == kDmma || kind == kDmmaP) && RPT * CW == 16 && CW == 8 && SB == 65536 &&
+  const bool swz = sizeof(T) == 8 && (kind == kDmma || kind == kDmmaP) && DmmaGeom<RPT, CW, SB>::swz_ok && SB == 65536 &&
                    (NT == 8 || NT == 16) && swz_layout_ok(A, m, k, lda);
   const size_t bt_bytes = align_up((size_t)kpad * NT * sizeof(T), 256);
   TSM2X_TRY(ws_reserve(ws, bt_bytes + acc_bytes, (size_t)it.num_rb + 8, s));
@@ -1047,11 +1060,14 @@ static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m,
       const char* e = getenv("TSM2X_STAGE_KB");
       return e ? atoi(e) : 64;
     }();
+    static const int env_rb = env_int("TSM2X_RB", 512);  // row-block height of the DMMA passes (experiment)
     if constexpr (sizeof(T) == 8 && (NT == 8 || NT == 16)) {
-      if (env_stage_kb == 64 && env_cw == 0 && env_rpt == 0)
+      if (env_stage_kb == 64 && env_cw == 0 && env_rpt == 0 && env_rb == 512)
         return run_tsm2r_tma<T, NT, 2, 8, 65536>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
       if (env_cw == 16 && env_rpt == 1)  // 16 consumer warps x 1 row: 512-row blocks (DMMA-capable)
         return run_tsm2r_tma<T, NT, 1, 16>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
+      if (env_rb == 1024 && env_stage_kb == 64)  // 16 warps x 64 rows: 1024-row blocks, 8 columns per stage
+        return run_tsm2r_tma<T, NT, 2, 16, 65536>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
     }
     if constexpr (sizeof(T) == 8 && NT == 8) {
       if (env_cw == 16) return run_tsm2r_tma<T, NT, 2, 16>(di, ws, m, k, w, A, lda, B, ldb, C, ldc, c_is_zero, ordered, s);
