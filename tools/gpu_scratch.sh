@@ -1,2 +1,2 @@
-timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/gputest.log 2>&1; tail -2 gpurun_out/gputest.log
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -6
+for n in 8 16; do python tools/gap_probe.py 30720 $n 20; python tools/gap_probe.py 30720 $n 20 det; done
+python tools/gap_probe.py 8192 8 50; python tools/gap_probe.py 8192 8 50 det
