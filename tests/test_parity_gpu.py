@@ -466,30 +466,35 @@ def test_config4_fp32_benchmarked_path_full():
 
 
 @pytest.mark.slow
-def test_config3_l_opt2_zero_c_benchmarked_path():
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_config3_l_opt2_zero_c_benchmarked_path(prec):
     """BASELINE config 3 as benchmarked: L_OPT2 (zero-C contract, C never read) at m = 2^24,
-    k = n = 16, fp64 — full result against cuBLAS DGEMM of the same inputs and sampled slabs
-    against the oracle. C starts as NaN so a read of C would show."""
+    k = n = 16 — fp64 (DMMA) and fp32 (FFMA2 single-chunk path with the direct-store epilogue):
+    full result against a float64 torch product of the same inputs and sampled slabs against the
+    oracle. C starts as NaN so a read of C would show."""
     import torch
     from oracle.rng import uniform_block
     tsm = _tsm()
+    dt = torch.float64 if prec == "double" else torch.float32
+    tol = 1e-12 if prec == "double" else 1e-5
     m, k, n = 1 << 24, 16, 16
-    A = tsm.colmajor_empty(m, k, torch.float64, "cuda")
+    A = tsm.colmajor_empty(m, k, dt, "cuda")
     tsm.fill_uniform(A, seed=17)
-    B = tsm.colmajor_empty(k, n, torch.float64, "cuda")
+    B = tsm.colmajor_empty(k, n, dt, "cuda")
     tsm.fill_uniform(B, seed=18)
-    C = tsm.colmajor_empty(m, n, torch.float64, "cuda")
+    C = tsm.colmajor_empty(m, n, dt, "cuda")
     C.fill_(float("nan"))  # c_is_zero: the kernel must not read it
     tsm.gemm(A, B, C, variant="l-opt2", c_is_zero=True)
     torch.cuda.synchronize()
-    full = A @ B
+    full = A.double() @ B.double()
     assert torch.isfinite(C).all()
-    assert rel_frobenius(C.cpu().numpy(), full.cpu().numpy()) <= 1e-12
-    Bh = uniform_block(range(k), range(n), 18)
+    assert rel_frobenius(C.double().cpu().numpy(), full.cpu().numpy()) <= tol
+    npdt = np.float64 if prec == "double" else np.float32
+    Bh = uniform_block(range(k), range(n), 18).astype(npdt)
     for r0 in (0, 5_000_017, m - 777):
         rows = range(r0, min(m, r0 + 777))
-        ref = naive_gemm(uniform_block(rows, range(k), 17), Bh, np.zeros((len(rows), n)))
-        _check(C[r0:r0 + len(rows)].cpu().numpy(), ref, k, "double", what=("l-opt2", r0))
+        ref = naive_gemm(uniform_block(rows, range(k), 17).astype(npdt), Bh, np.zeros((len(rows), n), npdt))
+        _check(C[r0:r0 + len(rows)].cpu().numpy(), ref, k, prec, what=("l-opt2", prec, r0))
 
 
 @pytest.mark.parametrize("consumer", ["fma", "dmma", "ffma2", "tc", "dmmap", "dmma/cw16", "fma/cw16", "auto/sb64",

@@ -1,2 +1,1 @@
-for n in 8 16; do python tools/gap_probe.py 30720 $n 20; python tools/gap_probe.py 30720 $n 20 det; done
-python tools/gap_probe.py 8192 8 50; python tools/gap_probe.py 8192 8 50 det
+timeout 900 python -m pytest tests/test_parity_gpu.py -m gpu -q -x -k "config3_l_opt2" 2>&1 | tail -2
