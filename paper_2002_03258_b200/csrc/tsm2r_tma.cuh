@@ -213,6 +213,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+__device__ __forceinline__ void red_add(float* p, float v) {
+  asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
 __device__ __forceinline__ void red_add(double* p, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
@@ -319,7 +322,10 @@ __device__ __forceinline__ void finish_item(const DynArgs<T>& a, int64_t rb, int
       if constexpr (sizeof(T) == 8) {
         if (row < a.m) red_add(reinterpret_cast<double*>(a.C) + j * a.ldc + row, (double)acc[r][j]);
       } else {
-        red_add(a.acc + j * a.ldacc + row, (double)acc[r][j]);  // accumulator padded to whole row blocks
+        if (a.acc)
+          red_add(a.acc + j * a.ldacc + row, (double)acc[r][j]);  // accumulator padded to whole row blocks
+        else if (row < a.m)  // small fp32 calls: fp32 reductions straight into C (one launch per call)
+          red_add(reinterpret_cast<float*>(a.C) + j * a.ldc + row, (float)acc[r][j]);
       }
     }
   }

@@ -466,6 +466,27 @@ static int pick_consumer_rt(size_t eb, int nt, bool split, const Tuning& tu) {
   return kFma;
 }
 
+// TSM2X_CONSUMER=tc in the environment (A/B runs, tests) forces the tensor cores everywhere
+static bool env_forces_tc() {
+  static const bool v = [] {
+    const char* e = getenv("TSM2X_CONSUMER");
+    return e && !strcmp(e, "tc");
+  }();
+  return v;
+}
+
+// "Small" calls (A <= 256 MB): launch-bound, so they take the single-launch variants (inline B;
+// fp32 reductions into C).
+static inline bool small_call(int64_t m, int64_t k, size_t eb) {
+  return (double)m * (double)k * (double)eb <= 256.0 * 1048576.0;
+}
+// fp32 C += calls up to 128 MB of A skip the tensor cores' three launches (prep, tc32, finalize)
+// for one FFMA2 launch with fp32 reductions into C: 512^2..4096^2 x 16 12-27 % faster, 8192^2
+// (256 MB) 6 % slower (tools/small_vs_cublas.py, profiles/small_vs_cublas_r02.jsonl)
+static inline bool f32_direct_call(int64_t m, int64_t k) {
+  return (double)m * (double)k * 4.0 <= 128.0 * 1048576.0;
+}
+
 // Whether an fp32 pass of width nt splits its row blocks into several column chunks (TSM2R) or
 // runs them as single chunks (TSM2L shapes), on the FFMA2 geometry (make_items below).
 static bool fp32_split(int sms, int64_t m, int64_t k, int nt);
@@ -692,7 +713,13 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   a.ldacc = (int64_t)it.num_rb * Cfg::R;
   a.ordered = ordered ? 1 : 0;
   const bool atomic_split = split && !a.ordered;
-  const size_t acc_bytes = (atomic_split && sizeof(T) == 4) ? (size_t)a.ldacc * NT * sizeof(double) : 0;
+  // fp32 split row blocks combine in an fp64 accumulator + tsm2_finalize — except small calls
+  // that read C (C += A*B, A <= 128 MB: a few column chunks per row block), which reduce in fp32
+  // straight into C: no accumulator to zero, no finalize, and with the inline-B producer one
+  // launch per call (fp32 512^2..4096^2 x 16 were launch-bound at three launches)
+  const bool f32_direct = sizeof(T) == 4 && atomic_split && !c_is_zero && f32_direct_call(m, k);
+  const bool f32_acc = sizeof(T) == 4 && atomic_split && !f32_direct;
+  const size_t acc_bytes = f32_acc ? (size_t)a.ldacc * NT * sizeof(double) : 0;
   int kind = pick_consumer_rt(sizeof(T), NT, split, tu);
   // DMMA: the 512-row geometries (8 warps x 2 rows or 16 warps x 1 row); FFMA2: the default one
   if ((kind == kDmma || kind == kDmmaP) && !DmmaGeom<RPT, CW, SB>::ok) kind = kFma;
@@ -712,7 +739,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   // contract, the fp64 accumulator for fp32), if any
   double* zp = nullptr;
   int64_t zld = 0, zrows = 0;
-  if (atomic_split && sizeof(T) == 4) {
+  if (f32_acc) {
     zp = a.acc;
     zld = zrows = a.ldacc;
   } else if (atomic_split && c_is_zero) {
@@ -728,8 +755,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
   // deep in the power-capped regime (> 1 s back to back) is it ~2 % ahead at n = 3..8.
   // TSM2X_INLINE_B = 0 never, 1 always, unset = this rule.
   static const int inline_env = env_int("TSM2X_INLINE_B", -1);
-  const bool want_inline =
-      inline_env == 1 || (inline_env < 0 && (double)m * (double)k * (double)eb <= 256.0 * 1048576.0);
+  const bool want_inline = inline_env == 1 || (inline_env < 0 && small_call(m, k, eb));
   if (!zp && want_inline) {
     a.inline_b = 1;
     a.B = B;
@@ -809,7 +835,7 @@ static int run_tsm2r_tma(const DevInfo& di, Workspace* ws, int64_t m, int64_t k,
             med[4], mx[4], (long long)G);
   }
 #endif
-  if (atomic_split && sizeof(T) == 4) {
+  if (f32_acc) {
     const int64_t tot = m * w;
     const unsigned grid = (unsigned)std::min<int64_t>((tot + 255) / 256, (int64_t)di.sms * 8);
     TSM2X_TRY(launch_finalize<T>(grid, a.acc, a.ldacc, C, ldc, m, w, a.c_is_zero, s));
@@ -1036,7 +1062,9 @@ static int run_tsm2r_pass(const DevInfo& di, Workspace* ws, int impl, int64_t m,
   if constexpr (sizeof(T) == 4 && (NT == 16 || NT == 8)) {
     // fp32: the tensor-core consumer when chosen (TSM2X_CONSUMER=tc / tuning consumer 4) and the
     // layout allows the 3-D TMA view; the deterministic (ordered) combine stays on FFMA2
+    // small C += calls stay on FFMA2 with fp32 reductions into C: one launch instead of three
     if (tma && !ordered && pick_consumer_rt(4, NT, fp32_split(di.sms, m, k, NT), current_tuning()) == kTc &&
+        !(f32_direct_call(m, k) && !c_is_zero && current_tuning().consumer != 4 && !env_forces_tc()) &&
         tc32_ok(reinterpret_cast<const float*>(A), m, k, lda))
       return run_tsm2r_tc32(di, ws, m, k, w, reinterpret_cast<const float*>(A), lda,
                             reinterpret_cast<const float*>(B), ldb, reinterpret_cast<float*>(C), ldc, c_is_zero, s);
@@ -2031,6 +2059,7 @@ int tsm2x_plan_for(int precision, int64_t m, int64_t k, int64_t n, int64_t lda, 
   Items it;
   int64_t G;
   if (eb == 4 && nt == 16 && !determ && tu.combine != 1 && pick_consumer_rt(4, nt, fp32_split(sms, m, k, nt), tu) == kTc &&
+      !(f32_direct_call(m, k) && !(flags & TSM2X_FLAG_C_IS_ZERO) && tu.consumer != 4 && !env_forces_tc()) &&
       a_aligned16 && lda % 4 == 0 && lda >= (int64_t)align_up((size_t)m, 32) && k < (int64_t(1) << 31)) {
     // fp32 16-column passes on the tensor cores (run_tsm2r_tc32)
     out->rows_per_block = Tc32Cfg::R;

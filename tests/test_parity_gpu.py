@@ -742,3 +742,26 @@ def test_tsm2l_splitn_against_oracle(prec, m, k, n, c_zero):
     ref = naive_gemm(uniform_block(range(m), range(k), 61).astype(npdt), uniform_block(range(k), range(n), 62).astype(npdt),
                      C0h)
     _check(C.cpu().numpy(), ref, k, prec, what=("splitn", m, k, n, c_zero))
+
+
+def test_fp32_small_direct_reductions():
+    """Small fp32 C += calls (A <= 128 MB) run as one FFMA2 launch whose split row blocks reduce in
+    fp32 straight into C (no fp64 accumulator, no finalize): C += A.B within the fp32 tolerance on
+    even, ragged and equal-split shapes, and C's prior contents are kept."""
+    import torch
+    tsm = _tsm()
+    from paper_2002_03258_b200 import tuning
+    rng = np.random.default_rng(23)
+    for (m, k, n) in [(512, 512, 16), (1024, 1024, 16), (4096, 4096, 16), (1000, 3000, 13), (2048, 5000, 8),
+                      (300, 20000, 16)]:
+        assert tuning.plan("single", m, k, n)["consumer"] == "ffma2", (m, k, n)
+        A = tsm.colmajor_empty(m, k, torch.float32, "cuda")
+        A.copy_(torch.from_numpy(rng.random((m, k)).astype(np.float32)))
+        B = tsm.colmajor_empty(k, n, torch.float32, "cuda")
+        B.copy_(torch.from_numpy(rng.random((k, n)).astype(np.float32)))
+        C0 = rng.random((m, n)).astype(np.float32) * 100
+        C = tsm.colmajor_empty(m, n, torch.float32, "cuda")
+        C.copy_(torch.from_numpy(C0))
+        tsm.gemm(A, B, C)
+        ref = C0.astype(np.float64) + A.cpu().numpy().astype(np.float64) @ B.cpu().numpy().astype(np.float64)
+        assert rel_frobenius(C.cpu().numpy().astype(np.float64), ref) <= 1e-5, (m, k, n)

@@ -49,8 +49,8 @@ def test_plan_midsize_one_item_per_cta(mk, n, prec):
 def test_plan_few_row_blocks_split():
     # fewer row blocks than CTAs: short-k shapes are split across CTAs too (fp32 512^2 x 16 used
     # to run on one CTA), while TSM2L shapes (k within one stage) stay single-chunk
-    p = tuning.plan("single", 512, 512, 16)
-    assert p["items"] == p["grid"] == 32 and p["nsmall"] == 32
+    p = tuning.plan("single", 512, 512, 16)  # small C += call: FFMA2, fp32 reductions into C
+    assert p["consumer"] == "ffma2" and p["items"] == p["grid"] == p["nsmall"] > 16
     p = tuning.plan("double", 1000, 200, 8)
     assert p["nsmall"] > 1 and p["grid"] == p["items"]
     p = tuning.plan("double", 4096, 16, 16)
