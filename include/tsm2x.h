@@ -20,7 +20,8 @@
  *   tsm2x_last_error <- the ValueError / RuntimeError message text.
  *
  * Return codes: 0 = OK; TSM2X_EINVAL maps to Python ValueError (same conditions as the
- * reference), every other negative code maps to RuntimeError. Messages are thread-local.
+ * reference, plus a device C that overlaps A or B in memory), every other negative code maps to
+ * RuntimeError. Messages are thread-local.
  * All entry points are re-entrant and thread-safe; device work is stream-ordered.
  */
 #ifndef TSM2X_H_

@@ -1212,6 +1212,17 @@ static int run_device(int variant, int64_t m, int64_t k, int64_t n, const T* A, 
     return fail(TSM2X_EINVAL, "leading dimensions too small: lda=%lld (m=%lld) ldb=%lld (k=%lld) ldc=%lld",
                 (long long)lda, (long long)m, (long long)ldb, (long long)k, (long long)ldc);
   if (!A || !B || !C) return fail(TSM2X_EINVAL, "null matrix pointer");
+  // C is written while A and B are read (A streamed, B gathered per stage): C must not overlap
+  // either (the reference's Matrix inputs are distinct immutable arrays)
+  {
+    auto span = [](const void* p, int64_t rows, int64_t cols, int64_t ld) {
+      const uintptr_t b = reinterpret_cast<uintptr_t>(p);
+      return std::make_pair(b, b + (uintptr_t)(((cols - 1) * ld + rows) * (int64_t)sizeof(T)));
+    };
+    const auto c = span(C, m, n, ldc), a = span(A, m, k, lda), b = span(B, k, n, ldb);
+    if ((c.first < a.second && a.first < c.second) || (c.first < b.second && b.first < c.second))
+      return fail(TSM2X_EINVAL, "C overlaps A or B in memory: C is written while A and B are read");
+  }
   Workspace* ws = workspace_for(dev, s);
   std::lock_guard<std::mutex> lk(ws->mu);
   bool c_is_zero = (flags & TSM2X_FLAG_C_IS_ZERO) != 0;

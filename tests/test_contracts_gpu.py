@@ -180,3 +180,24 @@ def test_release_cached_memory_frees_stream_workspaces():
     torch.cuda.synchronize()
     ref = (A.double() @ B.double())
     assert rel_frobenius(C.double().cpu().numpy(), ref.cpu().numpy()) <= 1e-5
+
+
+def test_overlapping_c_rejected():
+    """C is written while A and B are read: a C that overlaps A or B is a ValueError, with no
+    device work (a disjoint sub-view of the same buffer is fine)."""
+    import torch
+    import paper_2002_03258_b200 as tsm
+    buf = tsm.colmajor_empty(4096, 64, torch.float64, "cuda")
+    tsm.fill_uniform(buf, 1)
+    A = buf[:, 0:32]
+    B = tsm.colmajor_empty(32, 8, torch.float64, "cuda")
+    tsm.fill_uniform(B, 2)
+    with pytest.raises(ValueError, match="overlaps"):
+        tsm.gemm(A, B, buf[:, 24:32])  # C = the last 8 columns of A
+    with pytest.raises(ValueError, match="overlaps"):
+        tsm.gemm(buf[:32, 32:64], B, buf[:32, 40:48])
+    C = buf[:, 40:48]  # columns 40-47: disjoint from A (0-31)
+    ref = C.clone() + A @ B
+    tsm.gemm(A, B, C)
+    torch.cuda.synchronize()
+    assert torch.allclose(C, ref, rtol=1e-12, atol=0)
