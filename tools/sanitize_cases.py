@@ -21,7 +21,9 @@ CASES = [
     (1500, 1300, 16, torch.float64, {}),              # DMMA, ragged rows
     (3000, 16, 16, torch.float64, {"variant": "l-opt2", "c_is_zero": True}),  # TSM2L, single-chunk
     (2048, 1500, 8, torch.float64, {"deterministic": True}),                 # ordered tickets
-    (2048, 1500, 16, torch.float32, {}),              # tcgen05 split tf32
+    (2048, 1500, 16, torch.float32, {}),              # small fp32 C +=: FFMA2, fp32 reductions into C
+    (2048, 1500, 16, torch.float32, {"tc": True}),    # tcgen05 split tf32 (16 converter warps), fp64 acc + finalize
+    (2048, 1500, 16, torch.float32, {"c_is_zero": True}),  # fp32 split under zero-C: fp64 acc + finalize
     (3000, 16, 16, torch.float32, {"variant": "l-opt2", "c_is_zero": True}),  # FFMA2 single-chunk, direct stores
     (3000, 16, 16, torch.float32, {"variant": "l-opt2", "c_is_zero": True, "tc": True}),  # tc32 single-chunk (deferred epilogue)
     (3000, 20, 16, torch.float32, {}),                # FFMA2 single-chunk, C += (4-column C groups)
